@@ -1,0 +1,381 @@
+#!/usr/bin/env python
+"""ACP-SGD aggregation benchmark (BASELINE.json metric: "ACP-SGD aggregation
+ms/step & gradient GB/s, ResNet-50/BERT-L, 1-8 B200").
+
+One *step* = one acp_step() of Alg. 2 over a model's whole synthetic gradient
+set (orthogonalise -> fused EF + projection -> pack -> per-bucket NCCL
+all-reduce -> decode + residual), alternating P-/Q-steps. Gradients live in
+HBM before the timed region (uniform(-1,1)/sqrt(m) values; inputs larger than
+L2). value = whole-job gradient GB/s = N_gpus * 4 * elements / (ms/step),
+max over ranks.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload bert-large-r4]
+  torchrun --nproc-per-node N bench.py --gpus N ...
+  python bench.py --impl reference ...   (the CPU oracle on a bounded sample)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    "bert-large-r4": ("bert-large", 4),
+    "resnet50-r4": ("resnet50", 4),
+    "resnet152-r4": ("resnet152", 4),
+    "bert-base-r8": ("bert-base", 8),
+    "bert-large-r1": ("bert-large", 1),
+    "bert-large-r2": ("bert-large", 2),
+    "bert-large-r8": ("bert-large", 8),
+    "bert-large-r16": ("bert-large", 16),
+    "bert-large-r32": ("bert-large", 32),
+}
+METRIC = "ACP-SGD aggregation gradient GB/s (ms/step alongside), ResNet-50/BERT-L, 1-8 B200"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def _shapes(model):
+    from acp_inputs import ready_order
+    return [s for _, s in ready_order(model)]
+
+
+def _numel(s):
+    n = 1
+    for d in s:
+        n *= int(d)
+    return n
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons via NVML during the timed region."""
+
+    def __init__(self, device_index, period=0.01):
+        self.dev = device_index
+        self.period = period
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            self.N = N
+            self.h = N.nvmlDeviceGetHandleByIndex(self.dev)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+        except Exception:
+            self.N = None
+            return self
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def _run(self):
+        N = self.N
+        names = {
+            "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4,
+            "hw_slowdown": 0x8, "sync_boost": 0x10, "sw_thermal_slowdown": 0x20,
+            "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80,
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM))
+                r = N.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, v in names.items():
+                    if r & v and k != "gpu_idle":
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        med = statistics.median(self.samples) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def _cpu_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        info = threadpool_info()
+        return max(d.get("num_threads", 1) for d in info) if info else 1
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def oracle_sample(model, rank, frac_every=3):
+    """Bounded sample of the workload for the CPU oracle: every `frac_every`-th
+    matrix (ready order) plus all vectors."""
+    sh = _shapes(model)
+    return [s for i, s in enumerate(sh) if len(s) == 1 or i % frac_every == 0]
+
+
+def time_oracle(model, rank, steps, warmup, world=1, frac_every=3):
+    """Run the oracle (as it stands) on the bounded sample; returns GB/s."""
+    import numpy as np
+    from oracle import AcpOracle
+    sel = oracle_sample(model, rank, frac_every)
+    n = sum(_numel(s) for s in sel)
+    o = AcpOracle(sel, rank, world_size=world, seed=1)
+    rs = np.random.default_rng(0)
+    g = [[(rs.random(s, dtype=np.float32) * 2 - 1) for s in sel] for _ in range(world)]
+    for t in range(warmup):
+        o.step(g, t % 2)
+    t0 = time.perf_counter()
+    for t in range(steps):
+        o.step(g, (warmup + t) % 2)
+    dt = (time.perf_counter() - t0) / max(steps, 1)
+    return {"gbs": 4.0 * n / dt / 1e9, "s_per_step": dt, "elements": n, "tensors": len(sel)}
+
+
+def run_reference(args):
+    rank_env = int(os.environ.get("RANK", "0"))
+    if rank_env != 0:
+        return 0
+    model, r = WORKLOADS[args.workload]
+    res = time_oracle(model, r, args.steps, args.warmup, frac_every=args.oracle_every)
+    cores = _cpu_threads()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": res["gbs"], "unit": "GB/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * res["s_per_step"], "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.workload, "rank": r, "sample_elements": res["elements"],
+                   "sample_tensors": res["tensors"]},
+        "cpu_baseline": {"value": res["gbs"], "unit": "GB/s", "cores": cores, "kind": "oracle",
+                         "sample": f"{model} r={r}: every {args.oracle_every}rd matrix + all vectors "
+                                   f"({res['elements']} elements), one worker, numpy fp64"},
+        "e2e": {"value": res["gbs"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def _setup_dist(args):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def _measure(model, r, world, rank, local, args, comm, profile=True):
+    import torch
+    from paper_2306_08881_b200 import AcpContext
+    shapes = _shapes(model)
+    nel = sum(_numel(s) for s in shapes)
+    gen = torch.Generator(device="cuda").manual_seed(1000 + rank)
+    grads = []
+    for s in shapes:
+        m = _numel(s[1:]) if len(s) > 1 else 1
+        g = torch.rand(s, device="cuda", generator=gen) * 2 - 1
+        grads.append((g / (m ** 0.5)).contiguous())
+    ctx = AcpContext(shapes, r, world_size=world, nccl_comm=comm, seed=7,
+                     bucket_bytes=args.bucket_bytes)
+    stream = torch.cuda.current_stream()
+    for t in range(args.warmup):
+        ctx.step(grads, t % 2)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    if profile:
+        ctx.profile(True)
+        ctx.profile_reset()
+    l0 = ctx.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        ev0.record(stream)
+        for t in range(args.steps):
+            ctx.step(grads, (args.warmup + t) % 2)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+    launches = ctx.launch_count() - l0
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    prof = ctx.profile_read() if profile else None
+    ctx.profile(False)
+    nb = (len(ctx.buckets(0)), len(ctx.buckets(1)))
+    return {"ctx": ctx, "grads": grads, "shapes": shapes, "nel": nel, "ms": ms, "prof": prof,
+            "launches": launches, "clocks": clk.summary(), "buckets": nb}
+
+
+def _e2e(res, world, args):
+    """Same step through the public API with HOST buffers: pinned H2D of the
+    step's gradients, acp_step, D2H of the decoded gradients, all timed."""
+    import torch
+    ctx, grads = res["ctx"], res["grads"]
+    host_in = [g.detach().cpu().pin_memory() for g in grads]
+    host_out = [torch.empty_like(h).pin_memory() for h in host_in]
+    steps = max(2, min(args.steps, args.e2e_steps))
+    stream = torch.cuda.current_stream()
+
+    def one(t):
+        for h, g in zip(host_in, grads):
+            g.copy_(h, non_blocking=True)
+        ctx.step(grads, t % 2)
+        for g, h in zip(grads, host_out):
+            h.copy_(g, non_blocking=True)
+
+    one(0)
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        torch.distributed.barrier()
+    ev0.record(stream)
+    for t in range(steps):
+        one(t + 1)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / steps
+    if world > 1:
+        tt = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        ms = float(tt.item())
+    nbytes = 4 * res["nel"]
+    return {"value": world * nbytes / (ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": ms,
+            "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "steps": steps}
+
+
+def _roofline(prof, peak, peak_kind, workload):
+    cls = [k for k in ("proj_p", "proj_q", "decode_p", "decode_q") if prof[k]["launches"] > 0]
+    dom = max(cls, key=lambda k: prof[k]["ms"])
+    d = prof[dom]
+    per_launch_bytes = d["bytes"] / d["launches"]
+    per_launch_ms = d["ms"] / d["launches"]
+    achieved = per_launch_bytes / (per_launch_ms * 1e-3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            tr = json.load(f)
+        traffic = tr.get(workload, {}).get(dom)
+    except Exception:
+        pass
+    return {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
+            "algorithmic_bytes_per_launch": per_launch_bytes, "ms_per_launch": per_launch_ms,
+            "per_class": {k: {"ms_per_launch": v["ms"] / v["launches"],
+                              "gbs": (v["bytes"] / v["launches"]) / (v["ms"] / v["launches"] * 1e-3) / 1e9}
+                          for k, v in prof.items() if v["launches"] > 0}}
+
+
+def run_ours(args):
+    import torch
+    world, rank, local = _setup_dist(args)
+    if world != args.gpus:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+    comm = None
+    if world > 1:
+        from paper_2306_08881_b200 import nccl_comm_from_group
+        comm = nccl_comm_from_group()
+    model, r = WORKLOADS[args.workload]
+    res = _measure(model, r, world, rank, local, args, comm)
+    peak, peak_kind = _peaks()
+    ms = res["ms"]
+    nel = res["nel"]
+    value = world * 4.0 * nel / (ms * 1e-3) / 1e9
+    roof = _roofline(res["prof"], peak, peak_kind, args.workload)
+    e2e = _e2e(res, world, args) if not args.no_e2e else None
+    secondary = None
+    if args.secondary and args.secondary != args.workload:
+        res["ctx"].close()
+        del res["grads"]
+        torch.cuda.empty_cache()
+        m2, r2 = WORKLOADS[args.secondary]
+        s = _measure(m2, r2, world, rank, local, args, comm)
+        secondary = {"workload": args.secondary, "ms_per_step": s["ms"],
+                     "value": world * 4.0 * s["nel"] / (s["ms"] * 1e-3) / 1e9, "unit": "GB/s",
+                     "step_hbm_frac_16B": 16.0 * s["nel"] / (s["ms"] * 1e-3) / 1e9 / peak,
+                     "roofline": _roofline(s["prof"], peak, peak_kind, args.secondary),
+                     "gpu_launches": s["launches"]}
+        s["ctx"].close()
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cb = time_oracle(model, r, 2, 1, frac_every=args.oracle_every)
+        cpu = {"value": cb["gbs"], "unit": "GB/s", "cores": _cpu_threads(), "kind": "oracle",
+               "sample": f"{model} r={r}: every {args.oracle_every}rd matrix + all vectors "
+                         f"({cb['elements']} of {nel} elements), 1 warm + 2 timed steps (P,Q), numpy fp64"}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": args.workload, "model_shapes": model, "rank": r,
+                       "elements_per_gpu": nel, "parity": "alternating P/Q steps",
+                       "buckets_PQ": list(res["buckets"]) if world > 1 else [1, 1],
+                       "bucket_rule": f"{args.bucket_bytes} B x compression rate (P:257)",
+                       "l2": "inputs larger than L2 (M+E working set > 126 MB), no flush",
+                       "parallelism": f"dp{world}"},
+            "step_hbm_frac_16B": 16.0 * nel / (ms * 1e-3) / 1e9 / peak,
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": res["clocks"],
+            "gpu_launches": res["launches"],
+            "secondary": secondary,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="bert-large-r4", choices=sorted(WORKLOADS))
+    ap.add_argument("--secondary", default="resnet50-r4")
+    ap.add_argument("--bucket-bytes", type=int, default=25 * 2 ** 20)
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--oracle-every", type=int, default=3)
+    args = ap.parse_args(argv)
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,187 @@
+/*
+ * acp.h -- C ABI of the B200-native ACP-SGD hot path.
+ *
+ * ACP-SGD = "alternate compressed Power-SGD" with error feedback,
+ * Algorithm 2 of arXiv 2306.08881 ("Evaluation and Optimization of Gradient
+ * Compression for Distributed Deep Learning").
+ * "P:n" below is PAPER.md line n; "S:n" is SPEC.md line n; "C<k>" is a
+ * reading listed in DESIGN.md "Readings".
+ *
+ * One call of acp_step() runs, for EVERY tensor of a data-parallel worker's
+ * gradient set, one iteration of Alg. 2 (parity 0 = the paper's odd t,
+ * parity 1 = even t; C1):
+ *
+ *   parity 0 (P-step)          parity 1 (Q-step)
+ *   Q  <- Orthogonalize(Q_{t-1})          P  <- Orthogonalize(P_{t-1})
+ *   M' <- M + E_{t-1}                     M' <- M + E_{t-1}
+ *   P  <- M' Q            (local)         Q  <- M'^T P          (local)
+ *   E  <- M' - P Q^T      (local P, C3)   E  <- M' - P Q^T      (local Q, C3)
+ *   P  <- All-Reduce(P)   (sum, C2)       Q  <- All-Reduce(Q)   (sum, C2)
+ *   grad <- P Q^T / p         grad <- P Q^T / p
+ *
+ * 1-D tensors (biases, norms) are not compressed; they are copied into
+ * the same fused buffer as the fresh factors and all-reduced with them
+ * (P:257 numbers, C8): grad <- All-Reduce(grad) / p.
+ *
+ * Layout (all float32, little endian):
+ *   - gradient of tensor i: caller-owned, row-major n_i x m_i (n = dim0,
+ *     m = prod(dims[1:]), "reshaped into matrices", C9), overwritten in
+ *     place with the decoded (averaged) gradient;
+ *   - fused buffers ("P-buffer" used on parity 0, "Q-buffer" on parity 1):
+ *     one slot per tensor in READY order, slot i starting at a multiple of 4
+ *     floats (16 B) and padded to a multiple of 4 floats; a matrix slot holds
+ *     its fresh factor k-major (column k of P, n_i floats, then column k+1 ...;
+ *     resp. of Q, m_i floats each), a vector slot holds the vector;
+ *   - buckets (tensor fusion, C10): greedy in ready order, sealed
+ *     once their payload (4 * elements, unpadded) reaches
+ *     cap = max(1 KiB, ceil(default_bucket_bytes * rate_parity)),
+ *     rate_P = (sum n_i r_i + N_v)/N, rate_Q = (sum m_i r_i + N_v)/N; a bucket
+ *     is the contiguous float range of its slots (padding included);
+ *   - E: one float region per matrix (row-major n_i x m_i) in ready order,
+ *     each starting at a multiple of 4 floats.
+ *   r_i = min(rank, n_i, m_i) (C7).
+ *
+ * Ownership: the caller owns the gradients, the workspace (device memory of at
+ * least acp_workspace_bytes()), the CUDA stream and the NCCL communicator.
+ * The library allocates no device memory, keeps no gradient pointers across
+ * calls, and enqueues all device work asynchronously on the caller's stream
+ * (plus one internal stream used for the all-reduces when world_size > 1).
+ *
+ * Errors: functions return acp_status. ACP_E_INVAL means the arguments were
+ * rejected with no side effects; ACP_E_CUDA / ACP_E_NCCL poison the context
+ * and every later call on it returns ACP_E_STATE. acp_last_error() returns a
+ * thread-local description of the last non-OK status. Non-finite gradients
+ * pass through unchecked (as SPEC S:141 does for collectives). All ranks must
+ * issue identical parity sequences.
+ */
+#ifndef ACP_H
+#define ACP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ACP_ABI_VERSION 1
+
+typedef struct acp_ctx acp_ctx;
+
+typedef enum {
+  ACP_OK = 0,
+  ACP_E_INVAL = 1,  /* invalid argument or configuration; nothing changed   */
+  ACP_E_CUDA = 2,   /* a CUDA call failed; context poisoned                  */
+  ACP_E_NCCL = 3,   /* an NCCL call failed; context poisoned                 */
+  ACP_E_NOMEM = 4,  /* workspace smaller than acp_workspace_bytes()          */
+  ACP_E_STATE = 5   /* context poisoned by an earlier failure                */
+} acp_status;
+
+/* flags */
+enum {
+  ACP_NO_EF = 1u,     /* error feedback off: E == 0 (ablation, C12)      */
+  ACP_NO_REUSE = 2u,  /* query reuse off: orthogonalise a fresh seeded N(0,1)
+                         factor each step instead of the previous aggregated
+                         one (ablation, C12)                            */
+  ACP_SUM = 4u        /* decoded gradient = sum over workers (default: / p)   */
+};
+
+typedef struct {
+  int32_t abi_version;           /* ACP_ABI_VERSION                                    */
+  int32_t num_tensors;           /* >= 1, in READY order (reverse parameter order)     */
+  const int64_t* rows;           /* host, num_tensors: n_i = dim0 (vector: its length) */
+  const int64_t* cols;           /* host, num_tensors: m_i = prod(dims[1:]) >= 1, or
+                                    0 to mark a 1-D (vector) tensor of length rows[i]  */
+  int32_t rank;                  /* r >= 1; per tensor r_i = min(r, n_i, m_i)          */
+  int32_t world_size;            /* p >= 1 (divisor of the decoded gradient)           */
+  void* nccl_comm;               /* ncclComm_t of p ranks, required iff world_size > 1
+                                    and acp_step() is used (the split API needs none)  */
+  uint64_t seed;                 /* seeds the method's own draws (Q_0 when q0_host is
+                                    NULL, rank-deficiency repair, NO_REUSE); identical
+                                    on all ranks                                       */
+  const float* q0_host;          /* optional host array: for each matrix in ready order
+                                    its Q_0 (m_i x r_i, row-major), concatenated; NULL:
+                                    Q_0 from the counter-based generator   */
+  int64_t default_bucket_bytes;  /* 25 MiB in the paper; 0 = one tensor per
+                                    bucket; < 0 = a single bucket                      */
+  uint32_t flags;                /* ACP_NO_EF | ACP_NO_REUSE | ACP_SUM                 */
+  int32_t device;                /* CUDA device ordinal the context runs on            */
+  void* workspace;               /* device memory, >= acp_workspace_bytes()            */
+  size_t workspace_bytes;
+} acp_config;
+
+/* Bytes of device workspace the configuration needs (E + both fused buffers +
+ * scratch). Reads only the shape fields of *cfg. */
+acp_status acp_workspace_bytes(const acp_config* cfg, size_t* out_bytes);
+
+/* Build the plan, upload it into the workspace, write Q_0, zero E.
+ * Synchronous (returns after the device work is done). */
+acp_status acp_create(const acp_config* cfg, acp_ctx** out_ctx);
+
+/* One ACP-SGD step (see top). grads: host array of num_tensors DEVICE
+ * pointers, each to the tensor's fp32 contiguous gradient, overwritten with
+ * the decoded mean. parity: 0 = P-step, 1 = Q-step. cuda_stream: a
+ * cudaStream_t (NULL = legacy default stream). Asynchronous. */
+acp_status acp_step(acp_ctx* ctx, int32_t parity, float* const* grads, void* cuda_stream);
+
+/* Split API (simulated workers / external all-reduce): acp_compress runs the
+ * orthogonalisation and the fused projection + pack of ALL tensors and returns
+ * the parity's whole fused buffer (device pointer and float count); the caller
+ * replaces its contents by the element-wise SUM over workers; acp_decompress
+ * then decodes into grads. Both asynchronous on cuda_stream. */
+acp_status acp_compress(acp_ctx* ctx, int32_t parity, float* const* grads,
+                        float** out_buffer, int64_t* out_count, void* cuda_stream);
+acp_status acp_decompress(acp_ctx* ctx, int32_t parity, float* const* grads, void* cuda_stream);
+
+/* State of matrix tensor i (tests, checkpoint/resume). Device pointers; any
+ * may be NULL to skip. P: n_i x r_i row-major, Q: m_i x r_i row-major,
+ * E: n_i x m_i row-major. Asynchronous on cuda_stream. */
+acp_status acp_get_state(acp_ctx* ctx, int32_t tensor, float* P, float* Q, float* E,
+                         void* cuda_stream);
+acp_status acp_set_state(acp_ctx* ctx, int32_t tensor, const float* P, const float* Q,
+                         const float* E, void* cuda_stream);
+
+/* Plan of tensor i: out[0] = r_i (0 for vectors), out[1] = slot offset in the
+ * P-buffer (floats), out[2] = slot offset in the Q-buffer, out[3] = E offset
+ * (-1 for vectors), out[4] = P-bucket index, out[5] = Q-bucket index. */
+acp_status acp_plan_info(acp_ctx* ctx, int32_t tensor, int64_t out[6]);
+
+/* Number of buckets of a parity, and bucket b's [offset, count) in floats
+ * within that parity's fused buffer. */
+acp_status acp_num_buckets(acp_ctx* ctx, int32_t parity, int32_t* out);
+acp_status acp_bucket_range(acp_ctx* ctx, int32_t parity, int32_t bucket, int64_t* offset,
+                            int64_t* count);
+
+/* Kernel timing for roofline reporting. When enabled, every kernel launch is
+ * bracketed by CUDA events on its launching stream. acp_profile_read
+ * synchronises the context's streams and returns, for kernel class k
+ * (ACP_K_*), the summed event time (ms), the number of launches and the
+ * summed ALGORITHMIC bytes moved. Reset clears. */
+enum { ACP_K_ORTH = 0, ACP_K_PROJ_P = 1, ACP_K_PROJ_Q = 2, ACP_K_DECODE_P = 3,
+       ACP_K_DECODE_Q = 4, ACP_K_ALLREDUCE = 5, ACP_K_NUM = 6 };
+acp_status acp_profile_enable(acp_ctx* ctx, int32_t enable);
+acp_status acp_profile_reset(acp_ctx* ctx);
+acp_status acp_profile_read(acp_ctx* ctx, int32_t kernel_class, double* ms, int64_t* launches,
+                            double* algorithmic_bytes);
+
+/* Number of kernels this context has launched so far (its own kernels, not
+ * NCCL's). */
+acp_status acp_launch_count(acp_ctx* ctx, int64_t* out);
+
+acp_status acp_destroy(acp_ctx* ctx);
+
+/* thread-local description of the last non-OK status ("" if none) */
+const char* acp_last_error(void);
+int32_t acp_abi_version(void);
+
+/* NCCL bootstrap helpers (the caller broadcasts the 128-byte id over its own
+ * process group, e.g. torch.distributed, then every rank creates the comm). */
+acp_status acp_nccl_unique_id(uint8_t out_id[128]);
+acp_status acp_nccl_comm_create(const uint8_t id[128], int32_t nranks, int32_t rank,
+                                int32_t device, void** out_comm);
+acp_status acp_nccl_comm_destroy(void* comm);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ACP_H */

@@ -1,0 +1,11 @@
+"""B200-native ACP-SGD hot path (arXiv 2306.08881, Alg. 2).
+
+The compute path is ``lib/libacp.so`` (sm_100a kernels + NCCL) behind the C
+ABI in ``include/acp.h``; this package only marshals arguments. Importing it
+loads the library and fails loudly if it has not been built.
+"""
+from ._lib import (load as _load, AcpError, ACP_NO_EF, ACP_NO_REUSE, ACP_SUM,  # noqa: F401
+                   LIB_PATH, EXPORTED)
+from .acp import AcpContext, nccl_comm_from_group, nccl_comm_destroy, DEFAULT_BUCKET_BYTES  # noqa: F401
+
+_load()

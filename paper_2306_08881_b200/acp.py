@@ -1,0 +1,212 @@
+"""Python face of the C ABI: ``AcpContext`` (one data-parallel worker).
+
+PyTorch provides the device memory (workspace, gradients), the CUDA stream and
+the process group used to bootstrap NCCL; every step of the hot path runs in
+the library's sm_100a kernels and NCCL.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import _lib as L
+
+DEFAULT_BUCKET_BYTES = 25 * 2 ** 20
+
+
+def _shape_rows_cols(shapes):
+    rows, cols = [], []
+    for s in shapes:
+        s = tuple(int(d) for d in s)
+        if len(s) == 0:
+            raise ValueError("scalar tensors are not supported")
+        if len(s) == 1:
+            rows.append(s[0]); cols.append(0)            # vector: uncompressed
+        else:
+            rows.append(s[0]); cols.append(int(np.prod(s[1:])))  # n = dim0, m = prod(rest)
+    return rows, cols
+
+
+def _stream_handle(stream) -> int:
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return int(stream.cuda_stream)
+
+
+def nccl_comm_from_group(group=None, device: Optional[int] = None) -> int:
+    """Create an NCCL communicator spanning ``group`` (torch.distributed):
+    rank 0 draws the unique id, the group broadcasts it, every rank inits."""
+    import torch
+    import torch.distributed as dist
+    lib = L.load()
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    uid = (C.c_uint8 * 128)()
+    if rank == 0:
+        L.check(lib.acp_nccl_unique_id(uid))
+    payload = [bytes(uid)]
+    dist.broadcast_object_list(payload, src=dist.get_global_rank(group, 0) if group else 0,
+                               group=group)
+    uid = (C.c_uint8 * 128).from_buffer_copy(payload[0])
+    dev = torch.cuda.current_device() if device is None else device
+    comm = C.c_void_p()
+    L.check(lib.acp_nccl_comm_create(uid, world, rank, dev, C.byref(comm)))
+    return comm.value
+
+
+def nccl_comm_destroy(comm: int) -> None:
+    L.check(L.load().acp_nccl_comm_destroy(C.c_void_p(comm)))
+
+
+class AcpContext:
+    """ACP-SGD state of one worker for a list of parameter shapes in READY
+    order (the order gradients become ready in back-propagation)."""
+
+    def __init__(self, shapes: Sequence[Sequence[int]], rank: int, *, world_size: int = 1,
+                 nccl_comm: Optional[int] = None, seed: int = 0,
+                 q0: Optional[List[Optional[np.ndarray]]] = None,
+                 bucket_bytes: int = DEFAULT_BUCKET_BYTES, flags: int = 0,
+                 device=None):
+        import torch
+        self._lib = L.load()
+        self.shapes = [tuple(int(d) for d in s) for s in shapes]
+        self.rank = int(rank)
+        self.world_size = int(world_size)
+        dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self.device = dev
+        rows, cols = _shape_rows_cols(self.shapes)
+        T = len(rows)
+        self._rows = (C.c_int64 * T)(*rows)
+        self._cols = (C.c_int64 * T)(*cols)
+        cfg = L.AcpConfig()
+        cfg.abi_version = L.ACP_ABI_VERSION
+        cfg.num_tensors = T
+        cfg.rows = C.cast(self._rows, C.POINTER(C.c_int64))
+        cfg.cols = C.cast(self._cols, C.POINTER(C.c_int64))
+        cfg.rank = self.rank
+        cfg.world_size = self.world_size
+        cfg.nccl_comm = C.c_void_p(nccl_comm) if nccl_comm else None
+        cfg.seed = int(seed) & 0xFFFFFFFFFFFFFFFF
+        cfg.default_bucket_bytes = int(bucket_bytes)
+        cfg.flags = int(flags)
+        cfg.device = dev.index if dev.index is not None else torch.cuda.current_device()
+        q0buf = None
+        if q0 is not None:
+            parts = []
+            for s, q in zip(self.shapes, q0):
+                if len(s) == 1:
+                    continue
+                parts.append(np.ascontiguousarray(q, dtype=np.float32).ravel())
+            flat = np.concatenate(parts) if parts else np.zeros(1, np.float32)
+            q0buf = (C.c_float * flat.size).from_buffer_copy(flat.tobytes())
+            cfg.q0_host = C.cast(q0buf, C.POINTER(C.c_float))
+        nbytes = C.c_size_t()
+        L.check(self._lib.acp_workspace_bytes(C.byref(cfg), C.byref(nbytes)))
+        self.workspace = torch.empty(int(nbytes.value), dtype=torch.uint8, device=dev)
+        cfg.workspace = C.c_void_p(self.workspace.data_ptr())
+        cfg.workspace_bytes = nbytes.value
+        ctx = C.c_void_p()
+        L.check(self._lib.acp_create(C.byref(cfg), C.byref(ctx)))
+        self._ctx = ctx
+        self._cfg = cfg
+        self._ptrs = (C.c_void_p * T)()
+
+    # -- helpers --------------------------------------------------------------
+    def _grad_ptrs(self, grads):
+        import torch
+        if len(grads) != len(self.shapes):
+            raise ValueError(f"expected {len(self.shapes)} gradients, got {len(grads)}")
+        for i, (g, s) in enumerate(zip(grads, self.shapes)):
+            if not (isinstance(g, torch.Tensor) and g.is_cuda and g.dtype == torch.float32
+                    and g.is_contiguous() and g.numel() == int(np.prod(s))):
+                raise ValueError(f"gradient {i} must be a contiguous fp32 CUDA tensor of shape {s}")
+            self._ptrs[i] = g.data_ptr()
+        return C.cast(self._ptrs, C.POINTER(C.c_void_p))
+
+    # -- hot path -------------------------------------------------------------
+    def step(self, grads, parity: int, stream=None) -> None:
+        """One ACP-SGD step; grads are overwritten with the decoded mean."""
+        L.check(self._lib.acp_step(self._ctx, int(parity), self._grad_ptrs(grads),
+                                   C.c_void_p(_stream_handle(stream))))
+
+    def compress(self, grads, parity: int, stream=None):
+        """Split API: returns the parity's fused buffer as a torch view."""
+        import torch
+        buf = C.c_void_p()
+        cnt = C.c_int64()
+        L.check(self._lib.acp_compress(self._ctx, int(parity), self._grad_ptrs(grads),
+                                       C.byref(buf), C.byref(cnt),
+                                       C.c_void_p(_stream_handle(stream))))
+        base = self.workspace.data_ptr()
+        off = buf.value - base
+        return self.workspace[off:off + 4 * cnt.value].view(torch.float32)
+
+    def decompress(self, grads, parity: int, stream=None) -> None:
+        L.check(self._lib.acp_decompress(self._ctx, int(parity), self._grad_ptrs(grads),
+                                         C.c_void_p(_stream_handle(stream))))
+
+    # -- state / plan ---------------------------------------------------------
+    def get_state(self, i: int, stream=None):
+        import torch
+        n, m = self.shapes[i][0], int(np.prod(self.shapes[i][1:]))
+        r = self.plan_info(i)[0]
+        P = torch.empty((n, r), dtype=torch.float32, device=self.device)
+        Q = torch.empty((m, r), dtype=torch.float32, device=self.device)
+        E = torch.empty((n, m), dtype=torch.float32, device=self.device)
+        L.check(self._lib.acp_get_state(self._ctx, i, C.c_void_p(P.data_ptr()),
+                                        C.c_void_p(Q.data_ptr()), C.c_void_p(E.data_ptr()),
+                                        C.c_void_p(_stream_handle(stream))))
+        return P, Q, E
+
+    def set_state(self, i: int, P=None, Q=None, E=None, stream=None) -> None:
+        ptr = lambda t: C.c_void_p(t.data_ptr()) if t is not None else None
+        L.check(self._lib.acp_set_state(self._ctx, i, ptr(P), ptr(Q), ptr(E),
+                                        C.c_void_p(_stream_handle(stream))))
+
+    def plan_info(self, i: int) -> Tuple[int, int, int, int, int, int]:
+        out = (C.c_int64 * 6)()
+        L.check(self._lib.acp_plan_info(self._ctx, i, out))
+        return tuple(int(x) for x in out)
+
+    def buckets(self, parity: int) -> List[Tuple[int, int]]:
+        nb = C.c_int32()
+        L.check(self._lib.acp_num_buckets(self._ctx, parity, C.byref(nb)))
+        res = []
+        for b in range(nb.value):
+            off, cnt = C.c_int64(), C.c_int64()
+            L.check(self._lib.acp_bucket_range(self._ctx, parity, b, C.byref(off), C.byref(cnt)))
+            res.append((off.value, cnt.value))
+        return res
+
+    # -- profiling ------------------------------------------------------------
+    def profile(self, enable: bool = True) -> None:
+        L.check(self._lib.acp_profile_enable(self._ctx, 1 if enable else 0))
+
+    def profile_reset(self) -> None:
+        L.check(self._lib.acp_profile_reset(self._ctx))
+
+    def profile_read(self) -> dict:
+        out = {}
+        for k, name in enumerate(L.KERNEL_CLASS_NAMES):
+            ms, n, by = C.c_double(), C.c_int64(), C.c_double()
+            L.check(self._lib.acp_profile_read(self._ctx, k, C.byref(ms), C.byref(n), C.byref(by)))
+            out[name] = {"ms": ms.value, "launches": n.value, "bytes": by.value}
+        return out
+
+    def launch_count(self) -> int:
+        n = C.c_int64()
+        L.check(self._lib.acp_launch_count(self._ctx, C.byref(n)))
+        return n.value
+
+    def close(self) -> None:
+        if getattr(self, "_ctx", None):
+            self._lib.acp_destroy(self._ctx)
+            self._ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,104 @@
+// Internal declarations shared by the host runtime (acp_runtime.cpp) and the
+// sm_100a kernels. Not part of the ABI.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace acp {
+
+constexpr int kThreads = 256;          // every hot kernel runs 256-thread CTAs
+constexpr int kMaxV = 8;               // row kernel: float4 chunks per thread per row
+constexpr int kOrthRowsPerSeg = 1024;  // K2 work unit (factor rows)
+constexpr int kOrthChunk = 64;         // K2 smem staging (rows)
+
+// Per-tensor descriptor uploaded once (device copy of the plan).
+struct LayerDesc {
+  int64_t n, m;        // matrix n x m; vector: n = length, m = 0
+  int32_t r;           // r_i (0 for vectors)
+  int32_t mat;         // 1 matrix, 0 vector
+  int64_t e_off;       // float offset into E (matrices)
+  int64_t p_off;       // float offset of the slot in the P-buffer
+  int64_t q_off;       // float offset of the slot in the Q-buffer
+  int64_t ql_off;      // float offset into the local-Q copy (matrices)
+  int32_t G;           // row kernel: threads per row (0 = generic path)
+  int32_t V;           // row kernel: float4 chunks per thread per row
+  int32_t W;           // col kernel: columns per thread (4, 2 or 1)
+  int32_t pw;          // col kernel: panel width in columns (= 256 * W)
+  int64_t w_off;       // K2: offset (doubles) of this layer's two r x r W matrices
+  int32_t deg_idx;     // K2: index into the degenerate-mask / counter arrays
+  int32_t pad_;
+};
+
+// Row-kernel work unit: rows [row0, row1) of matrix `layer`, or elements
+// [row0, row1) of vector `layer`.
+struct RowSeg {
+  int32_t layer;
+  int32_t pad_;
+  int64_t row0, row1;
+};
+
+// Column-kernel (K1 Q-step) work unit: rows [row0, row1) of panel `panel` of
+// matrix `layer`; writes its partial slot (r x pw floats at part_off); the
+// panel's pcount partial slots are contiguous and the last segment of the
+// panel to finish sums them in order into the Q slot (completion counter
+// `counter`). Vectors: pack elements [row0, row1).
+struct ColSeg {
+  int32_t layer;
+  int32_t panel;
+  int64_t row0, row1;
+  int64_t part_off;    // float offset of this segment's partial slot
+  int32_t pidx;        // index of this segment's partial among its panel's
+  int32_t pcount;      // number of partials of (layer, panel), contiguous
+  int32_t counter;     // completion counter of (layer, panel)
+  int32_t pad_;
+};
+
+// K2 (orthogonalisation) work unit: rows [row0, row1) of factor `layer`
+// (the Q factor on P-steps, the P factor on Q-steps).
+struct OrthSeg {
+  int32_t layer;
+  int32_t seg;         // index of this segment among the layer's segments
+  int64_t row0, row1;
+  int64_t gram_off;    // double offset of this segment's partial Gram (r x r)
+  int32_t nseg;        // segments of this layer
+  int32_t gram_first;  // segment index of the layer's first partial (gram_off of seg 0)
+};
+
+struct Tables {
+  const LayerDesc* layers;
+  float* const* grads;   // device table of gradient pointers
+  float* E;
+  float* pbuf;
+  float* qbuf;
+  float* qloc;
+  float* colpart;
+  int32_t* colcnt;
+  double* gram;
+  double* wmat;
+  int32_t* orthcnt;
+  uint32_t* degmask;
+};
+
+// launches (all on `stream`, 256 threads, grid = ncta)
+// mode 0: K1 P-step (projection + residual + pack into P-buffer)
+// mode 1: K3 P-step decode (+ unpack from P-buffer)
+// mode 2: K3 Q-step residual + decode (+ unpack from Q-buffer)
+cudaError_t launch_row(int mode, int rt, const Tables& t, const RowSeg* segs,
+                       const int32_t* cta_begin, int ncta, float scale, int ef,
+                       cudaStream_t stream);
+// K1 Q-step: column projection into the Q-buffer + local-Q copy (+ pack)
+cudaError_t launch_col(int rt, const Tables& t, const ColSeg* segs, const int32_t* cta_begin,
+                       int ncta, int ef, cudaStream_t stream);
+// K2: CholeskyQR2 of the factors named by segs (side 0: Q factors in the
+// Q-buffer, length m; side 1: P factors in the P-buffer, length n).
+cudaError_t launch_orth(int rt, const Tables& t, int side, const OrthSeg* segs, int nseg,
+                        uint64_t seed, int64_t step, cudaStream_t stream, int* launches);
+// Fill factor slots with counter-based N(0,1) (tag, step): side as above, or
+// side 2 = Q_0 into the Q-buffer. Layers = all matrices.
+cudaError_t launch_fill(const Tables& t, const LayerDesc* host_layers, int num_tensors, int side,
+                        uint64_t seed, int tag, int64_t step, cudaStream_t stream, int* launches);
+// k-major slot <-> row-major rows x r (state access)
+cudaError_t launch_transpose(const float* src, float* dst, int64_t rows, int r, int to_kmajor,
+                             cudaStream_t stream);
+
+}  // namespace acp

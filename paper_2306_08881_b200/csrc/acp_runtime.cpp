@@ -1,0 +1,872 @@
+// Host runtime behind include/acp.h: plan (shape policy, ranks, fused-buffer
+// layout, buckets, byte-balanced work lists), fused-buffer scheduler
+// (per-bucket projection -> NCCL all-reduce on a comm stream -> decode), and
+// the C ABI. See DESIGN.md for the layout and the readings it implements.
+#include "acp.h"
+#include "acp_internal.h"
+
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+namespace acp {
+int row_rows_per_iter(int mode, int V, int rt);
+}
+
+using namespace acp;
+
+namespace {
+
+thread_local std::string g_err;
+
+acp_status fail(acp_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+inline int64_t round4(int64_t x) { return (x + 3) / 4 * 4; }
+inline size_t align256(size_t x) { return (x + 255) / 256 * 256; }
+
+constexpr int kMaxRank = 32;
+
+struct Launch {
+  int64_t seg_off = 0;   // first segment (row or col array)
+  int64_t cb_off = 0;    // first entry of cta_begin
+  int ncta = 0;
+  double bytes = 0;      // algorithmic bytes moved by this launch
+};
+
+struct Unit {
+  int layer;
+  int panel;             // col kernel panel (-1 otherwise)
+  int64_t count;         // rows (matrix) or elements (vector)
+  double cost;           // bytes per row / element
+  int64_t align;         // preferred split granularity
+};
+
+struct Plan {
+  int T = 0, RT = 1, nsm = 148, nmat = 0;
+  bool ef = true;
+  std::vector<LayerDesc> L;
+  int64_t N = 0, e_elems = 0, arena[2] = {0, 0}, ql_elems = 0, wmat_elems = 0;
+  std::vector<std::vector<int>> buckets[2];
+  std::vector<int64_t> boff[2], bcnt[2];
+  std::vector<int> bucket_of[2];
+  std::vector<int64_t> payload[2];
+  std::vector<RowSeg> rowsegs;
+  std::vector<ColSeg> colsegs;
+  std::vector<OrthSeg> orthsegs[2];
+  std::vector<int32_t> ctab;
+  Launch k1_all[2], k3_all[2];
+  std::vector<Launch> k1_b[2], k3_b[2];
+  double orth_bytes[2] = {0, 0};
+  int64_t colpart_elems = 0, colcnt_n = 1, gram_elems = 1;
+  // workspace byte offsets
+  size_t off_E = 0, off_P = 0, off_Q = 0, off_QL = 0, off_colpart = 0, off_colcnt = 0,
+         off_gram = 0, off_wmat = 0, off_orthcnt = 0, off_degmask = 0, off_layers = 0,
+         off_grads = 0, off_rowsegs = 0, off_colsegs = 0, off_orth[2] = {0, 0}, off_ctab = 0,
+         total = 0;
+};
+
+// Split `units` into `grid` contiguous, cost-balanced CTA ranges of segments.
+template <class Emit>
+int split_units(const std::vector<Unit>& units, double min_share, int max_grid,
+                std::vector<int32_t>& ctab, Emit emit) {
+  double total = 0;
+  for (const Unit& u : units) total += u.cost * (double)u.count;
+  if (total <= 0) {
+    ctab.push_back(0);
+    return 0;
+  }
+  int grid = (int)std::ceil(total / min_share);
+  grid = std::max(1, std::min(grid, max_grid));
+  const double share = total / grid;
+  const size_t cb0 = ctab.size();
+  int nseg = 0;
+  ctab.push_back(0);
+  int cta = 0;
+  double done = 0;
+  for (const Unit& u : units) {
+    int64_t pos = 0;
+    while (pos < u.count) {
+      const double budget = share * (cta + 1) - done;
+      int64_t take = (int64_t)std::ceil(budget / u.cost);
+      take = (take + u.align - 1) / u.align * u.align;
+      if (take < 1) take = 1;
+      take = std::min(take, u.count - pos);
+      emit(u, pos, pos + take);
+      ++nseg;
+      done += u.cost * (double)take;
+      pos += take;
+      if (done >= share * (cta + 1) - 1e-6 * share && cta < grid - 1) {
+        ++cta;
+        ctab.push_back(nseg);
+      }
+    }
+  }
+  while ((int)(ctab.size() - cb0) < grid + 1) ctab.push_back(nseg);
+  return grid;
+}
+
+acp_status build_plan(const acp_config* cfg, Plan& P) {
+  if (!cfg) return fail(ACP_E_INVAL, "config is NULL");
+  if (cfg->abi_version != ACP_ABI_VERSION) return fail(ACP_E_INVAL, "abi_version mismatch");
+  if (cfg->num_tensors < 1) return fail(ACP_E_INVAL, "num_tensors must be >= 1");
+  if (!cfg->rows || !cfg->cols) return fail(ACP_E_INVAL, "rows/cols are NULL");
+  if (cfg->rank < 1) return fail(ACP_E_INVAL, "rank must be >= 1");
+  if (cfg->rank > kMaxRank) return fail(ACP_E_INVAL, "rank > 32 is not supported");
+  if (cfg->world_size < 1) return fail(ACP_E_INVAL, "world_size must be >= 1");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || cfg->device < 0 || cfg->device >= ndev)
+    return fail(ACP_E_INVAL, "invalid CUDA device");
+  int nsm = 0;
+  if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, cfg->device) != cudaSuccess)
+    return fail(ACP_E_CUDA, "cannot query SM count");
+  P.nsm = nsm;
+  P.T = cfg->num_tensors;
+  P.ef = !(cfg->flags & ACP_NO_EF);
+  P.L.assign(P.T, LayerDesc{});
+  int rmax = 1;
+  for (int i = 0; i < P.T; ++i) {
+    LayerDesc& L = P.L[i];
+    const int64_t n = cfg->rows[i], m = cfg->cols[i];
+    if (n < 1 || m < 0) return fail(ACP_E_INVAL, "tensor " + std::to_string(i) + ": bad shape");
+    L.n = n;
+    L.m = m;
+    L.mat = m > 0 ? 1 : 0;
+    L.r = L.mat ? (int)std::min<int64_t>(cfg->rank, std::min(n, m)) : 0;
+    L.deg_idx = i;
+    rmax = std::max(rmax, L.r);
+    P.N += L.mat ? n * m : n;
+    if (L.mat) ++P.nmat;
+  }
+  while (P.RT < rmax) P.RT <<= 1;
+  // offsets
+  int64_t e = 0, ql = 0, w = 0, so[2] = {0, 0};
+  for (int p = 0; p < 2; ++p) P.payload[p].resize(P.T);
+  for (int i = 0; i < P.T; ++i) {
+    LayerDesc& L = P.L[i];
+    P.payload[0][i] = L.mat ? L.n * L.r : L.n;
+    P.payload[1][i] = L.mat ? L.m * L.r : L.n;
+    L.p_off = so[0];
+    L.q_off = so[1];
+    so[0] += round4(P.payload[0][i]);
+    so[1] += round4(P.payload[1][i]);
+    if (L.mat) {
+      L.e_off = e;
+      e += round4(L.n * L.m);
+      L.ql_off = ql;
+      ql += round4(L.m * L.r);
+      L.w_off = w;
+      w += 2LL * L.r * L.r;
+      // row kernel thread-group shape
+      L.G = 0;
+      L.V = 0;
+      if (L.m % 4 == 0 && L.m / 4 <= (int64_t)kThreads * kMaxV) {
+        const int64_t m4 = L.m / 4;
+        double best = 1e30;
+        for (int G = kThreads; G >= 1; G >>= 1) {
+          const int64_t V = (m4 + G - 1) / G;
+          if (V > kMaxV) continue;
+          const double score = (double)(G * V - m4) / (double)(G * V) + 0.02 * std::abs((double)V - 4.0);
+          if (score < best) {
+            best = score;
+            L.G = G;
+            L.V = (int)V;
+          }
+        }
+      }
+      L.W = (L.m % 4 == 0 && P.RT <= 8) ? 4 : ((L.m % 2 == 0 && P.RT <= 16) ? 2 : 1);
+      L.pw = kThreads * L.W;
+    } else {
+      L.e_off = -1;
+      L.ql_off = -1;
+      L.w_off = -1;
+    }
+  }
+  P.e_elems = e;
+  P.ql_elems = ql;
+  P.wmat_elems = std::max<int64_t>(w, 1);
+  P.arena[0] = so[0];
+  P.arena[1] = so[1];
+  // buckets per parity (greedy, seal when >= cap)
+  for (int p = 0; p < 2; ++p) {
+    int64_t F = 0;
+    for (int i = 0; i < P.T; ++i) F += P.payload[p][i];
+    const double rate = (double)F / (double)P.N;
+    int64_t cap = cfg->default_bucket_bytes;
+    if (cap > 0) cap = std::max<int64_t>(1024, (int64_t)std::ceil((double)cap * rate));
+    P.bucket_of[p].assign(P.T, 0);
+    std::vector<int> cur;
+    int64_t tot = 0;
+    for (int i = 0; i < P.T; ++i) {
+      cur.push_back(i);
+      tot += 4 * P.payload[p][i];
+      if (cap >= 0 && tot >= cap) {
+        P.buckets[p].push_back(cur);
+        cur.clear();
+        tot = 0;
+      }
+    }
+    if (!cur.empty()) P.buckets[p].push_back(cur);
+    for (size_t b = 0; b < P.buckets[p].size(); ++b) {
+      const int first = P.buckets[p][b].front(), last = P.buckets[p][b].back();
+      const int64_t off = p == 0 ? P.L[first].p_off : P.L[first].q_off;
+      const int64_t end = (p == 0 ? P.L[last].p_off : P.L[last].q_off) + round4(P.payload[p][last]);
+      P.boff[p].push_back(off);
+      P.bcnt[p].push_back(end - off);
+      for (int i : P.buckets[p][b]) P.bucket_of[p][i] = (int)b;
+    }
+  }
+
+  // ---- work lists ----
+  const int max_grid = nsm * 8;
+  const double min_share = 256.0 * 1024;
+  const bool ef = P.ef;
+  auto row_launch = [&](int mode, const std::vector<int>& tensors) {
+    std::vector<Unit> units;
+    double bytes = 0;
+    for (int i : tensors) {
+      const LayerDesc& L = P.L[i];
+      if (!L.mat) {
+        units.push_back({i, -1, L.n, 8.0, 1024});
+        bytes += 8.0 * L.n;
+        continue;
+      }
+      const double bpe = mode == 0 ? (ef ? 12.0 : 4.0) : (mode == 1 ? 4.0 : (ef ? 16.0 : 8.0));
+      int64_t align = 1;
+      if (L.G > 0) align = (int64_t)(kThreads / L.G) * row_rows_per_iter(mode, L.V, P.RT);
+      units.push_back({i, -1, L.n, bpe * (double)L.m, align});
+      // algorithmic bytes: M/E stream + factor traffic (each factor touched once)
+      bytes += bpe * (double)L.n * (double)L.m;
+      if (mode == 0) bytes += 4.0 * L.r * (double)(L.m + L.n);
+      if (mode == 1) bytes += 4.0 * L.r * (double)(L.m + L.n);
+      if (mode == 2) bytes += 4.0 * L.r * (double)(2 * L.m + L.n);
+    }
+    Launch ln;
+    ln.seg_off = (int64_t)P.rowsegs.size();
+    ln.cb_off = (int64_t)P.ctab.size();
+    ln.ncta = split_units(units, min_share, max_grid, P.ctab, [&](const Unit& u, int64_t a, int64_t b) {
+      RowSeg s{};
+      s.layer = u.layer;
+      s.row0 = a;
+      s.row1 = b;
+      P.rowsegs.push_back(s);
+    });
+    // cta_begin entries are relative to the launch's first segment
+    ln.bytes = bytes;
+    return ln;
+  };
+  auto col_launch = [&](const std::vector<int>& tensors) {
+    std::vector<Unit> units;
+    double bytes = 0;
+    int counters = 0;
+    for (int i : tensors) {
+      const LayerDesc& L = P.L[i];
+      if (!L.mat) {
+        units.push_back({i, -1, L.n, 8.0, 1024});
+        bytes += 8.0 * L.n;
+        continue;
+      }
+      const int64_t npan = (L.m + L.pw - 1) / L.pw;
+      for (int64_t pn = 0; pn < npan; ++pn) {
+        const int64_t pcols = std::min<int64_t>(L.pw, L.m - pn * L.pw);
+        units.push_back({i, (int)pn, L.n, (ef ? 8.0 : 4.0) * (double)pcols, 16});
+      }
+      bytes += (ef ? 8.0 : 4.0) * (double)L.n * (double)L.m + 4.0 * L.r * (double)(L.n + 2 * L.m);
+    }
+    Launch ln;
+    ln.seg_off = (int64_t)P.colsegs.size();
+    ln.cb_off = (int64_t)P.ctab.size();
+    int64_t part = 0;
+    int prev_layer = -1, prev_panel = -1;
+    size_t panel_first = 0;
+    auto close_panel = [&]() {
+      if (prev_layer < 0) return;
+      const int cnt = (int)(P.colsegs.size() - panel_first);
+      for (size_t k = panel_first; k < P.colsegs.size(); ++k) P.colsegs[k].pcount = cnt;
+    };
+    ln.ncta = split_units(units, min_share, max_grid, P.ctab, [&](const Unit& u, int64_t a, int64_t b) {
+      ColSeg s{};
+      s.layer = u.layer;
+      s.panel = u.panel;
+      s.row0 = a;
+      s.row1 = b;
+      if (u.panel >= 0) {
+        if (u.layer != prev_layer || u.panel != prev_panel) {
+          close_panel();
+          prev_layer = u.layer;
+          prev_panel = u.panel;
+          panel_first = P.colsegs.size();
+          ++counters;
+        }
+        s.counter = counters - 1;
+        s.pidx = (int)(P.colsegs.size() - panel_first);
+        s.part_off = part;
+        part += (int64_t)P.L[u.layer].r * P.L[u.layer].pw;
+      } else {
+        close_panel();
+        prev_layer = -1;
+        prev_panel = -1;
+        s.counter = -1;
+      }
+      P.colsegs.push_back(s);
+    });
+    close_panel();
+    P.colpart_elems = std::max(P.colpart_elems, part);
+    P.colcnt_n = std::max<int64_t>(P.colcnt_n, counters);
+    ln.bytes = bytes;
+    return ln;
+  };
+  std::vector<int> all(P.T);
+  for (int i = 0; i < P.T; ++i) all[i] = i;
+  P.k1_all[0] = row_launch(0, all);
+  P.k3_all[0] = row_launch(1, all);
+  P.k1_all[1] = col_launch(all);
+  P.k3_all[1] = row_launch(2, all);
+  if (cfg->world_size > 1) {
+    for (int p = 0; p < 2; ++p) {
+      for (const auto& b : P.buckets[p]) {
+        P.k1_b[p].push_back(p == 0 ? row_launch(0, b) : col_launch(b));
+        P.k3_b[p].push_back(row_launch(p == 0 ? 1 : 2, b));
+      }
+    }
+  }
+  // K2 segments per side (0: Q factors, length m; 1: P factors, length n)
+  for (int side = 0; side < 2; ++side) {
+    int64_t g = 0;
+    double bytes = 0;
+    for (int i = 0; i < P.T; ++i) {
+      const LayerDesc& L = P.L[i];
+      if (!L.mat) continue;
+      const int64_t len = side == 0 ? L.m : L.n;
+      const int nseg = (int)((len + kOrthRowsPerSeg - 1) / kOrthRowsPerSeg);
+      for (int j = 0; j < nseg; ++j) {
+        OrthSeg s{};
+        s.layer = i;
+        s.seg = j;
+        s.row0 = (int64_t)j * kOrthRowsPerSeg;
+        s.row1 = std::min<int64_t>(len, s.row0 + kOrthRowsPerSeg);
+        s.gram_off = g;
+        s.nseg = nseg;
+        g += (int64_t)L.r * L.r;
+        P.orthsegs[side].push_back(s);
+      }
+      bytes += 4.0 * L.r * (double)len * 5.0;  // read, read+write, read+write
+    }
+    P.gram_elems = std::max<int64_t>(P.gram_elems, g);
+    P.orth_bytes[side] = bytes;
+  }
+  // workspace layout
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    const size_t at = o;
+    o = align256(o + std::max<size_t>(bytes, 1));
+    return at;
+  };
+  P.off_E = take(4 * (size_t)P.e_elems);
+  P.off_P = take(4 * (size_t)P.arena[0]);
+  P.off_Q = take(4 * (size_t)P.arena[1]);
+  P.off_QL = take(4 * (size_t)P.ql_elems);
+  P.off_colpart = take(4 * (size_t)std::max<int64_t>(P.colpart_elems, 1));
+  P.off_colcnt = take(4 * (size_t)P.colcnt_n);
+  P.off_gram = take(8 * (size_t)P.gram_elems);
+  P.off_wmat = take(8 * (size_t)P.wmat_elems);
+  P.off_orthcnt = take(4 * (size_t)P.T);
+  P.off_degmask = take(4 * (size_t)P.T);
+  P.off_layers = take(sizeof(LayerDesc) * P.L.size());
+  P.off_grads = take(8 * (size_t)P.T);
+  P.off_rowsegs = take(sizeof(RowSeg) * P.rowsegs.size());
+  P.off_colsegs = take(sizeof(ColSeg) * P.colsegs.size());
+  P.off_orth[0] = take(sizeof(OrthSeg) * P.orthsegs[0].size());
+  P.off_orth[1] = take(sizeof(OrthSeg) * P.orthsegs[1].size());
+  P.off_ctab = take(4 * P.ctab.size());
+  P.total = o;
+  return ACP_OK;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+struct ProfRec {
+  int cls;
+  cudaEvent_t a, b;
+  double bytes;
+};
+
+}  // namespace
+
+struct acp_ctx {
+  acp_config cfg{};
+  Plan P;
+  char* ws = nullptr;
+  Tables tab{};
+  cudaStream_t comm_stream = nullptr;
+  std::vector<cudaEvent_t> ev_k1, ev_ar;
+  std::vector<float*> grads_cache;
+  int64_t step_count = 0;
+  int64_t launches = 0;
+  bool poisoned = false;
+  bool profile = false;
+  std::vector<ProfRec> prof;
+  size_t prof_used = 0;
+  ncclComm_t comm = nullptr;
+};
+
+namespace {
+
+acp_status cuda_fail(acp_ctx* c, cudaError_t e, const char* what) {
+  if (c) c->poisoned = true;
+  return fail(ACP_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(ctx, call, what)                          \
+  do {                                               \
+    cudaError_t e_ = (call);                         \
+    if (e_ != cudaSuccess) return cuda_fail(ctx, e_, what); \
+  } while (0)
+
+ProfRec* prof_begin(acp_ctx* c, int cls, double bytes, cudaStream_t s) {
+  if (!c->profile) return nullptr;
+  if (c->prof_used == c->prof.size()) {
+    ProfRec r{};
+    cudaEventCreate(&r.a);
+    cudaEventCreate(&r.b);
+    c->prof.push_back(r);
+  }
+  ProfRec* r = &c->prof[c->prof_used++];
+  r->cls = cls;
+  r->bytes = bytes;
+  cudaEventRecord(r->a, s);
+  return r;
+}
+void prof_end(ProfRec* r, cudaStream_t s) {
+  if (r) cudaEventRecord(r->b, s);
+}
+
+const RowSeg* dev_rowsegs(acp_ctx* c, const Launch& ln) {
+  return reinterpret_cast<const RowSeg*>(c->ws + c->P.off_rowsegs) + ln.seg_off;
+}
+const ColSeg* dev_colsegs(acp_ctx* c, const Launch& ln) {
+  return reinterpret_cast<const ColSeg*>(c->ws + c->P.off_colsegs) + ln.seg_off;
+}
+const int32_t* dev_ctab(acp_ctx* c, const Launch& ln) {
+  return reinterpret_cast<const int32_t*>(c->ws + c->P.off_ctab) + ln.cb_off;
+}
+
+float decode_scale(acp_ctx* c) {
+  return (c->cfg.flags & ACP_SUM) ? 1.0f : 1.0f / (float)c->cfg.world_size;
+}
+
+acp_status run_k1(acp_ctx* c, int parity, const Launch& ln, cudaStream_t s) {
+  if (ln.ncta <= 0) return ACP_OK;
+  const int ef = c->P.ef ? 1 : 0;
+  ProfRec* r = prof_begin(c, parity == 0 ? ACP_K_PROJ_P : ACP_K_PROJ_Q, ln.bytes, s);
+  cudaError_t e;
+  if (parity == 0)
+    e = launch_row(0, c->P.RT, c->tab, dev_rowsegs(c, ln), dev_ctab(c, ln), ln.ncta, 1.0f, ef, s);
+  else
+    e = launch_col(c->P.RT, c->tab, dev_colsegs(c, ln), dev_ctab(c, ln), ln.ncta, ef, s);
+  prof_end(r, s);
+  if (e != cudaSuccess) return cuda_fail(c, e, "projection kernel launch");
+  ++c->launches;
+  return ACP_OK;
+}
+
+acp_status run_k3(acp_ctx* c, int parity, const Launch& ln, cudaStream_t s) {
+  if (ln.ncta <= 0) return ACP_OK;
+  const int ef = c->P.ef ? 1 : 0;
+  ProfRec* r = prof_begin(c, parity == 0 ? ACP_K_DECODE_P : ACP_K_DECODE_Q, ln.bytes, s);
+  cudaError_t e = launch_row(parity == 0 ? 1 : 2, c->P.RT, c->tab, dev_rowsegs(c, ln),
+                             dev_ctab(c, ln), ln.ncta, decode_scale(c), ef, s);
+  prof_end(r, s);
+  if (e != cudaSuccess) return cuda_fail(c, e, "decode kernel launch");
+  ++c->launches;
+  return ACP_OK;
+}
+
+acp_status run_orth(acp_ctx* c, int parity, cudaStream_t s) {
+  const int side = parity == 0 ? 0 : 1;  // P-step orthogonalises Q, Q-step P
+  int nl = 0;
+  if (c->cfg.flags & ACP_NO_REUSE) {
+    cudaError_t e = launch_fill(c->tab, c->P.L.data(), c->P.T, side, c->cfg.seed, 3,
+                                c->step_count, s, &nl);
+    if (e != cudaSuccess) return cuda_fail(c, e, "fill kernel launch");
+  }
+  const auto& segs = c->P.orthsegs[side];
+  ProfRec* r = prof_begin(c, ACP_K_ORTH, c->P.orth_bytes[side], s);
+  cudaError_t e = launch_orth(c->P.RT, c->tab, side,
+                              reinterpret_cast<const OrthSeg*>(c->ws + c->P.off_orth[side]),
+                              (int)segs.size(), c->cfg.seed, c->step_count, s, &nl);
+  prof_end(r, s);
+  c->launches += nl;
+  if (e != cudaSuccess) return cuda_fail(c, e, "orthogonalisation kernel launch");
+  return ACP_OK;
+}
+
+acp_status set_grads(acp_ctx* c, float* const* grads, cudaStream_t s) {
+  if (!grads) return fail(ACP_E_INVAL, "grads is NULL");
+  bool same = true;
+  for (int i = 0; i < c->P.T; ++i) {
+    if (!grads[i]) return fail(ACP_E_INVAL, "grads[" + std::to_string(i) + "] is NULL");
+    if (grads[i] != c->grads_cache[i]) same = false;
+  }
+  if (same) return ACP_OK;
+  for (int i = 0; i < c->P.T; ++i) c->grads_cache[i] = grads[i];
+  // pageable source: staged before return, so the cache can change afterwards
+  CK(c, cudaMemcpyAsync(c->ws + c->P.off_grads, c->grads_cache.data(), 8 * (size_t)c->P.T,
+                        cudaMemcpyHostToDevice, s), "gradient table upload");
+  return ACP_OK;
+}
+
+acp_status check_ctx(acp_ctx* c) {
+  if (!c) return fail(ACP_E_INVAL, "ctx is NULL");
+  if (c->poisoned) return fail(ACP_E_STATE, "context poisoned by an earlier failure");
+  return ACP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t acp_abi_version(void) { return ACP_ABI_VERSION; }
+
+const char* acp_last_error(void) { return g_err.c_str(); }
+
+acp_status acp_workspace_bytes(const acp_config* cfg, size_t* out) {
+  if (!out) return fail(ACP_E_INVAL, "out is NULL");
+  Plan P;
+  acp_status st = build_plan(cfg, P);
+  if (st != ACP_OK) return st;
+  *out = P.total;
+  return ACP_OK;
+}
+
+acp_status acp_create(const acp_config* cfg, acp_ctx** out) {
+  if (!out) return fail(ACP_E_INVAL, "out is NULL");
+  *out = nullptr;
+  acp_ctx* c = new acp_ctx();
+  acp_status st = build_plan(cfg, c->P);
+  if (st != ACP_OK) {
+    delete c;
+    return st;
+  }
+  if (!cfg->workspace) {
+    delete c;
+    return fail(ACP_E_INVAL, "workspace is NULL");
+  }
+  if (cfg->workspace_bytes < c->P.total) {
+    delete c;
+    return fail(ACP_E_NOMEM, "workspace too small: need " + std::to_string(c->P.total) + " bytes");
+  }
+  if (cfg->world_size > 1 && !cfg->nccl_comm) {
+    // allowed: split API only; acp_step will reject
+  }
+  c->cfg = *cfg;
+  c->cfg.rows = nullptr;
+  c->cfg.cols = nullptr;
+  c->cfg.q0_host = nullptr;
+  c->comm = reinterpret_cast<ncclComm_t>(cfg->nccl_comm);
+  c->ws = reinterpret_cast<char*>(cfg->workspace);
+  c->grads_cache.assign(c->P.T, nullptr);
+  Plan& P = c->P;
+  Tables& t = c->tab;
+  t.layers = reinterpret_cast<const LayerDesc*>(c->ws + P.off_layers);
+  t.grads = reinterpret_cast<float* const*>(c->ws + P.off_grads);
+  t.E = reinterpret_cast<float*>(c->ws + P.off_E);
+  t.pbuf = reinterpret_cast<float*>(c->ws + P.off_P);
+  t.qbuf = reinterpret_cast<float*>(c->ws + P.off_Q);
+  t.qloc = reinterpret_cast<float*>(c->ws + P.off_QL);
+  t.colpart = reinterpret_cast<float*>(c->ws + P.off_colpart);
+  t.colcnt = reinterpret_cast<int32_t*>(c->ws + P.off_colcnt);
+  t.gram = reinterpret_cast<double*>(c->ws + P.off_gram);
+  t.wmat = reinterpret_cast<double*>(c->ws + P.off_wmat);
+  t.orthcnt = reinterpret_cast<int32_t*>(c->ws + P.off_orthcnt);
+  t.degmask = reinterpret_cast<uint32_t*>(c->ws + P.off_degmask);
+
+  DeviceGuard dg(cfg->device);
+  cudaStream_t s = nullptr;
+  auto bail = [&](cudaError_t e, const char* what) {
+    if (s) cudaStreamDestroy(s);
+    delete c;
+    return fail(ACP_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  };
+  cudaError_t e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return bail(e, "stream create");
+  if ((e = cudaMemsetAsync(c->ws, 0, P.total, s)) != cudaSuccess) return bail(e, "workspace memset");
+  auto up = [&](size_t off, const void* src, size_t bytes) {
+    return bytes ? cudaMemcpyAsync(c->ws + off, src, bytes, cudaMemcpyHostToDevice, s) : cudaSuccess;
+  };
+  if ((e = up(P.off_layers, P.L.data(), sizeof(LayerDesc) * P.L.size())) != cudaSuccess ||
+      (e = up(P.off_rowsegs, P.rowsegs.data(), sizeof(RowSeg) * P.rowsegs.size())) != cudaSuccess ||
+      (e = up(P.off_colsegs, P.colsegs.data(), sizeof(ColSeg) * P.colsegs.size())) != cudaSuccess ||
+      (e = up(P.off_orth[0], P.orthsegs[0].data(), sizeof(OrthSeg) * P.orthsegs[0].size())) != cudaSuccess ||
+      (e = up(P.off_orth[1], P.orthsegs[1].data(), sizeof(OrthSeg) * P.orthsegs[1].size())) != cudaSuccess ||
+      (e = up(P.off_ctab, P.ctab.data(), 4 * P.ctab.size())) != cudaSuccess)
+    return bail(e, "plan upload");
+  // Q_0: caller-provided (row-major m x r per matrix) or generated
+  std::vector<float> q0;
+  if (cfg->q0_host) {
+    q0.assign(P.arena[1], 0.f);
+    int64_t src = 0;
+    for (int i = 0; i < P.T; ++i) {
+      const LayerDesc& L = P.L[i];
+      if (!L.mat) continue;
+      for (int64_t j = 0; j < L.m; ++j)
+        for (int k = 0; k < L.r; ++k) q0[L.q_off + (int64_t)k * L.m + j] = cfg->q0_host[src + j * L.r + k];
+      src += L.m * L.r;
+    }
+    if ((e = up(P.off_Q, q0.data(), 4 * q0.size())) != cudaSuccess) return bail(e, "Q0 upload");
+  } else {
+    int nl = 0;
+    if ((e = launch_fill(t, P.L.data(), P.T, 2, cfg->seed, 1, 0, s, &nl)) != cudaSuccess)
+      return bail(e, "Q0 generator");
+  }
+  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return bail(e, "create sync");
+  cudaStreamDestroy(s);
+  s = nullptr;
+  if (cfg->world_size > 1) {
+    if ((e = cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking)) != cudaSuccess)
+      return bail(e, "comm stream");
+    const size_t nb = std::max(P.buckets[0].size(), P.buckets[1].size());
+    c->ev_k1.resize(nb);
+    c->ev_ar.resize(nb);
+    for (size_t b = 0; b < nb; ++b) {
+      cudaEventCreateWithFlags(&c->ev_k1[b], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&c->ev_ar[b], cudaEventDisableTiming);
+    }
+  }
+  *out = c;
+  g_err.clear();
+  return ACP_OK;
+}
+
+acp_status acp_step(acp_ctx* c, int32_t parity, float* const* grads, void* stream) {
+  acp_status st = check_ctx(c);
+  if (st != ACP_OK) return st;
+  if (parity != 0 && parity != 1) return fail(ACP_E_INVAL, "parity must be 0 or 1");
+  if (c->cfg.world_size > 1 && !c->comm)
+    return fail(ACP_E_INVAL, "world_size > 1 needs an NCCL communicator (or use the split API)");
+  DeviceGuard dg(c->cfg.device);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if ((st = set_grads(c, grads, s)) != ACP_OK) return st;
+  if ((st = run_orth(c, parity, s)) != ACP_OK) return st;
+  const Plan& P = c->P;
+  if (c->cfg.world_size == 1) {
+    if ((st = run_k1(c, parity, P.k1_all[parity], s)) != ACP_OK) return st;
+    if ((st = run_k3(c, parity, P.k3_all[parity], s)) != ACP_OK) return st;
+  } else {
+    float* buf = parity == 0 ? c->tab.pbuf : c->tab.qbuf;
+    const size_t nb = P.buckets[parity].size();
+    for (size_t b = 0; b < nb; ++b) {
+      if ((st = run_k1(c, parity, P.k1_b[parity][b], s)) != ACP_OK) return st;
+      CK(c, cudaEventRecord(c->ev_k1[b], s), "event record");
+      CK(c, cudaStreamWaitEvent(c->comm_stream, c->ev_k1[b], 0), "stream wait");
+      ProfRec* r = prof_begin(c, ACP_K_ALLREDUCE, 4.0 * P.bcnt[parity][b], c->comm_stream);
+      ncclResult_t nr = ncclAllReduce(buf + P.boff[parity][b], buf + P.boff[parity][b],
+                                      (size_t)P.bcnt[parity][b], ncclFloat, ncclSum, c->comm,
+                                      c->comm_stream);
+      prof_end(r, c->comm_stream);
+      if (nr != ncclSuccess) {
+        c->poisoned = true;
+        return fail(ACP_E_NCCL, std::string("ncclAllReduce: ") + ncclGetErrorString(nr));
+      }
+      CK(c, cudaEventRecord(c->ev_ar[b], c->comm_stream), "event record");
+    }
+    for (size_t b = 0; b < nb; ++b) {
+      CK(c, cudaStreamWaitEvent(s, c->ev_ar[b], 0), "stream wait");
+      if ((st = run_k3(c, parity, P.k3_b[parity][b], s)) != ACP_OK) return st;
+    }
+  }
+  ++c->step_count;
+  return ACP_OK;
+}
+
+acp_status acp_compress(acp_ctx* c, int32_t parity, float* const* grads, float** out_buffer,
+                        int64_t* out_count, void* stream) {
+  acp_status st = check_ctx(c);
+  if (st != ACP_OK) return st;
+  if (parity != 0 && parity != 1) return fail(ACP_E_INVAL, "parity must be 0 or 1");
+  if (!out_buffer || !out_count) return fail(ACP_E_INVAL, "output pointers are NULL");
+  DeviceGuard dg(c->cfg.device);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if ((st = set_grads(c, grads, s)) != ACP_OK) return st;
+  if ((st = run_orth(c, parity, s)) != ACP_OK) return st;
+  if ((st = run_k1(c, parity, c->P.k1_all[parity], s)) != ACP_OK) return st;
+  *out_buffer = parity == 0 ? c->tab.pbuf : c->tab.qbuf;
+  *out_count = c->P.arena[parity];
+  ++c->step_count;
+  return ACP_OK;
+}
+
+acp_status acp_decompress(acp_ctx* c, int32_t parity, float* const* grads, void* stream) {
+  acp_status st = check_ctx(c);
+  if (st != ACP_OK) return st;
+  if (parity != 0 && parity != 1) return fail(ACP_E_INVAL, "parity must be 0 or 1");
+  DeviceGuard dg(c->cfg.device);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if ((st = set_grads(c, grads, s)) != ACP_OK) return st;
+  return run_k3(c, parity, c->P.k3_all[parity], s);
+}
+
+acp_status acp_get_state(acp_ctx* c, int32_t i, float* Pm, float* Qm, float* Em, void* stream) {
+  acp_status st = check_ctx(c);
+  if (st != ACP_OK) return st;
+  if (i < 0 || i >= c->P.T || !c->P.L[i].mat) return fail(ACP_E_INVAL, "not a matrix tensor");
+  DeviceGuard dg(c->cfg.device);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const LayerDesc& L = c->P.L[i];
+  if (Pm) CK(c, launch_transpose(c->tab.pbuf + L.p_off, Pm, L.n, L.r, 0, s), "state transpose");
+  if (Qm) CK(c, launch_transpose(c->tab.qbuf + L.q_off, Qm, L.m, L.r, 0, s), "state transpose");
+  if (Em) CK(c, cudaMemcpyAsync(Em, c->tab.E + L.e_off, 4 * (size_t)(L.n * L.m),
+                               cudaMemcpyDeviceToDevice, s), "state copy");
+  return ACP_OK;
+}
+
+acp_status acp_set_state(acp_ctx* c, int32_t i, const float* Pm, const float* Qm, const float* Em,
+                         void* stream) {
+  acp_status st = check_ctx(c);
+  if (st != ACP_OK) return st;
+  if (i < 0 || i >= c->P.T || !c->P.L[i].mat) return fail(ACP_E_INVAL, "not a matrix tensor");
+  DeviceGuard dg(c->cfg.device);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const LayerDesc& L = c->P.L[i];
+  if (Pm) CK(c, launch_transpose(Pm, c->tab.pbuf + L.p_off, L.n, L.r, 1, s), "state transpose");
+  if (Qm) CK(c, launch_transpose(Qm, c->tab.qbuf + L.q_off, L.m, L.r, 1, s), "state transpose");
+  if (Em) CK(c, cudaMemcpyAsync(c->tab.E + L.e_off, Em, 4 * (size_t)(L.n * L.m),
+                               cudaMemcpyDeviceToDevice, s), "state copy");
+  return ACP_OK;
+}
+
+acp_status acp_plan_info(acp_ctx* c, int32_t i, int64_t out[6]) {
+  if (!c) return fail(ACP_E_INVAL, "ctx is NULL");
+  if (i < 0 || i >= c->P.T || !out) return fail(ACP_E_INVAL, "bad tensor index");
+  const LayerDesc& L = c->P.L[i];
+  out[0] = L.r;
+  out[1] = L.p_off;
+  out[2] = L.q_off;
+  out[3] = L.mat ? L.e_off : -1;
+  out[4] = c->P.bucket_of[0][i];
+  out[5] = c->P.bucket_of[1][i];
+  return ACP_OK;
+}
+
+acp_status acp_num_buckets(acp_ctx* c, int32_t parity, int32_t* out) {
+  if (!c || !out || (parity != 0 && parity != 1)) return fail(ACP_E_INVAL, "bad arguments");
+  *out = (int32_t)c->P.buckets[parity].size();
+  return ACP_OK;
+}
+
+acp_status acp_bucket_range(acp_ctx* c, int32_t parity, int32_t b, int64_t* off, int64_t* cnt) {
+  if (!c || !off || !cnt || (parity != 0 && parity != 1) || b < 0 ||
+      b >= (int32_t)c->P.buckets[parity].size())
+    return fail(ACP_E_INVAL, "bad arguments");
+  *off = c->P.boff[parity][b];
+  *cnt = c->P.bcnt[parity][b];
+  return ACP_OK;
+}
+
+acp_status acp_profile_enable(acp_ctx* c, int32_t enable) {
+  if (!c) return fail(ACP_E_INVAL, "ctx is NULL");
+  c->profile = enable != 0;
+  return ACP_OK;
+}
+
+acp_status acp_profile_reset(acp_ctx* c) {
+  if (!c) return fail(ACP_E_INVAL, "ctx is NULL");
+  c->prof_used = 0;
+  return ACP_OK;
+}
+
+acp_status acp_profile_read(acp_ctx* c, int32_t cls, double* ms, int64_t* launches, double* bytes) {
+  if (!c || !ms || !launches || !bytes || cls < 0 || cls >= ACP_K_NUM)
+    return fail(ACP_E_INVAL, "bad arguments");
+  DeviceGuard dg(c->cfg.device);
+  double tot = 0, by = 0;
+  int64_t n = 0;
+  for (size_t k = 0; k < c->prof_used; ++k) {
+    ProfRec& r = c->prof[k];
+    if (r.cls != cls) continue;
+    CK(c, cudaEventSynchronize(r.b), "profile event sync");
+    float t = 0;
+    CK(c, cudaEventElapsedTime(&t, r.a, r.b), "profile elapsed");
+    tot += t;
+    by += r.bytes;
+    ++n;
+  }
+  *ms = tot;
+  *launches = n;
+  *bytes = by;
+  return ACP_OK;
+}
+
+acp_status acp_launch_count(acp_ctx* c, int64_t* out) {
+  if (!c || !out) return fail(ACP_E_INVAL, "bad arguments");
+  *out = c->launches;
+  return ACP_OK;
+}
+
+acp_status acp_destroy(acp_ctx* c) {
+  if (!c) return ACP_OK;
+  DeviceGuard dg(c->cfg.device);
+  if (c->comm_stream) {
+    cudaStreamSynchronize(c->comm_stream);
+    cudaStreamDestroy(c->comm_stream);
+  }
+  for (auto ev : c->ev_k1) cudaEventDestroy(ev);
+  for (auto ev : c->ev_ar) cudaEventDestroy(ev);
+  for (auto& r : c->prof) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  delete c;
+  return ACP_OK;
+}
+
+acp_status acp_nccl_unique_id(uint8_t out_id[128]) {
+  if (!out_id) return fail(ACP_E_INVAL, "out is NULL");
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) return fail(ACP_E_NCCL, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  std::memcpy(out_id, &id, 128);
+  return ACP_OK;
+}
+
+acp_status acp_nccl_comm_create(const uint8_t id_bytes[128], int32_t nranks, int32_t rank,
+                                int32_t device, void** out) {
+  if (!id_bytes || !out || nranks < 1 || rank < 0 || rank >= nranks)
+    return fail(ACP_E_INVAL, "bad arguments");
+  DeviceGuard dg(device);
+  ncclUniqueId id;
+  std::memcpy(&id, id_bytes, 128);
+  ncclComm_t comm = nullptr;
+  ncclResult_t r = ncclCommInitRank(&comm, nranks, id, rank);
+  if (r != ncclSuccess) return fail(ACP_E_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+  *out = comm;
+  return ACP_OK;
+}
+
+acp_status acp_nccl_comm_destroy(void* comm) {
+  if (!comm) return ACP_OK;
+  ncclResult_t r = ncclCommDestroy(reinterpret_cast<ncclComm_t>(comm));
+  if (r != ncclSuccess) return fail(ACP_E_NCCL, std::string("ncclCommDestroy: ") + ncclGetErrorString(r));
+  return ACP_OK;
+}
+
+}  // extern "C"
