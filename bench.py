@@ -128,8 +128,15 @@ def _cpu_threads():
 def oracle_sample(model, rank, frac_every=3):
     """Bounded sample of the workload for the CPU oracle: every `frac_every`-th
     matrix (ready order) plus all vectors."""
-    sh = _shapes(model)
-    return [s for i, s in enumerate(sh) if len(s) == 1 or i % frac_every == 0]
+    out, k = [], 0
+    for s in _shapes(model):
+        if len(s) == 1:
+            out.append(s)
+        else:
+            if k % frac_every == 0:
+                out.append(s)
+            k += 1
+    return out
 
 
 def time_oracle(model, rank, steps, warmup, world=1, frac_every=3):
@@ -165,7 +172,7 @@ def run_reference(args):
         "config": {"workload": args.workload, "rank": r, "sample_elements": res["elements"],
                    "sample_tensors": res["tensors"]},
         "cpu_baseline": {"value": res["gbs"], "unit": "GB/s", "cores": cores, "kind": "oracle",
-                         "sample": f"{model} r={r}: every {args.oracle_every}rd matrix + all vectors "
+                         "sample": f"{model} r={r}: every {args.oracle_every}-th matrix + all vectors "
                                    f"({res['elements']} elements), one worker, numpy fp64"},
         "e2e": {"value": res["gbs"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -311,7 +318,7 @@ def run_ours(args):
     roof = _roofline(res["prof"], peak, peak_kind, args.workload)
     e2e = _e2e(res, world, args) if not args.no_e2e else None
     secondary = None
-    if args.secondary and args.secondary != args.workload:
+    if args.secondary and args.secondary not in ("none", args.workload):
         res["ctx"].close()
         del res["grads"]
         torch.cuda.empty_cache()
@@ -327,7 +334,7 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = time_oracle(model, r, 2, 1, frac_every=args.oracle_every)
         cpu = {"value": cb["gbs"], "unit": "GB/s", "cores": _cpu_threads(), "kind": "oracle",
-               "sample": f"{model} r={r}: every {args.oracle_every}rd matrix + all vectors "
+               "sample": f"{model} r={r}: every {args.oracle_every}-th matrix + all vectors "
                          f"({cb['elements']} of {nel} elements), 1 warm + 2 timed steps (P,Q), numpy fp64"}
     if rank == 0:
         line = {
