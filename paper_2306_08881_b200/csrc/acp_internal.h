@@ -26,7 +26,24 @@ struct LayerDesc {
   int32_t pw;          // col kernel: panel width in columns (= 256 * W)
   int64_t w_off;       // K2: offset (doubles) of this layer's two r x r W matrices
   int32_t deg_idx;     // K2: index into the degenerate-mask / counter arrays
-  int32_t pad_;
+  uint32_t fast;       // stream kernels: bulk-path eligibility (bit0 K1-P, bit1 K3-Q, bit2 K1-Q)
+  int32_t tr;          // stream row kernels: tile rows (multiple of 256 / G)
+  int32_t gc;          // stream col kernel: threads per row
+  int32_t vc;          // stream col kernel: float4 chunks per thread per row
+  int32_t trc;         // stream col kernel: tile rows
+};
+
+// Stream-kernel work unit: rows [row0, row1) of matrix `layer` (or elements of
+// a vector). Column mode: the segment writes `nslot` partial slots (r x m
+// floats each, k-major) starting at part_off; the layer's `pcount` slots are
+// contiguous and slot index of this segment's first one is `pidx`.
+struct StreamSeg {
+  int32_t layer;
+  int32_t nslot;
+  int64_t row0, row1;
+  int64_t part_off;
+  int32_t pidx;
+  int32_t pcount;
 };
 
 // Row-kernel work unit: rows [row0, row1) of matrix `layer`, or elements
@@ -89,6 +106,13 @@ cudaError_t launch_row(int mode, int rt, const Tables& t, const RowSeg* segs,
 // K1 Q-step: column projection into the Q-buffer + local-Q copy (+ pack)
 cudaError_t launch_col(int rt, const Tables& t, const ColSeg* segs, const int32_t* cta_begin,
                        int ncta, int ef, cudaStream_t stream);
+// TMA-pipelined streaming kernels (k_stream.cu): mode 0 K1 P-step, mode 2 K3
+// Q-step, mode 3 K1 Q-step. rt <= 8, error feedback on.
+cudaError_t launch_stream(int mode, int rt, const Tables& t, const StreamSeg* segs,
+                          const int32_t* cta_begin, int ncta, float scale, int stages,
+                          int stage_floats, cudaStream_t stream);
+bool stream_v_ok(int mode, int V, int rt);
+size_t stream_smem_bytes(int stages, int stage_floats);
 // K2: CholeskyQR2 of the factors named by segs (side 0: Q factors in the
 // Q-buffer, length m; side 1: P factors in the P-buffer, length n).
 cudaError_t launch_orth(int rt, const Tables& t, int side, const OrthSeg* segs, int nseg,

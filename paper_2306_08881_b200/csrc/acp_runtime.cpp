@@ -35,9 +35,12 @@ inline size_t align256(size_t x) { return (x + 255) / 256 * 256; }
 constexpr int kMaxRank = 32;
 
 struct Launch {
-  int64_t seg_off = 0;   // first segment (row or col array)
+  int kind = 0;          // 0 register row kernel, 1 register col kernel, 2 TMA stream kernel
+  int mode = 0;          // row: 0/1/2; stream: 0/2/3
+  int64_t seg_off = 0;   // first segment (row, col or stream array)
   int64_t cb_off = 0;    // first entry of cta_begin
   int ncta = 0;
+  int stages = 0, stage_floats = 0;
   double bytes = 0;      // algorithmic bytes moved by this launch
 };
 
@@ -60,6 +63,7 @@ struct Plan {
   std::vector<int64_t> payload[2];
   std::vector<RowSeg> rowsegs;
   std::vector<ColSeg> colsegs;
+  std::vector<StreamSeg> streamsegs;
   std::vector<OrthSeg> orthsegs[2];
   std::vector<int32_t> ctab;
   Launch k1_all[2], k3_all[2];
@@ -69,7 +73,8 @@ struct Plan {
   // workspace byte offsets
   size_t off_E = 0, off_P = 0, off_Q = 0, off_QL = 0, off_colpart = 0, off_colcnt = 0,
          off_gram = 0, off_wmat = 0, off_orthcnt = 0, off_degmask = 0, off_layers = 0,
-         off_grads = 0, off_rowsegs = 0, off_colsegs = 0, off_orth[2] = {0, 0}, off_ctab = 0,
+         off_grads = 0, off_rowsegs = 0, off_colsegs = 0, off_streamsegs = 0, off_orth[2] = {0, 0},
+         off_ctab = 0,
          total = 0;
 };
 
@@ -183,6 +188,33 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
       }
       L.W = (L.m % 4 == 0 && P.RT <= 8) ? 4 : ((L.m % 2 == 0 && P.RT <= 16) ? 2 : 1);
       L.pw = kThreads * L.W;
+      // TMA stream kernels: tiles of whole rows (one bulk copy per tensor)
+      L.fast = 0;
+      L.tr = L.trc = 0;
+      L.gc = L.vc = 0;
+      if (P.RT <= 8 && L.m % 4 == 0) {
+        const int64_t m4 = L.m / 4;
+        const int64_t target = 4096;  // floats per tile per tensor (16 KB)
+        if (L.G > 0 && L.V <= 5) {
+          const int NG = kThreads / L.G;
+          int64_t rr = std::max<int64_t>(1, target / ((int64_t)NG * L.m));
+          L.tr = (int)(NG * rr);
+          if (stream_v_ok(0, L.V, P.RT)) L.fast |= 1u;
+          if (stream_v_ok(2, L.V, P.RT)) L.fast |= 2u;
+        }
+        // column kernel prefers one row per 256 threads (one partial slot)
+        int gc = 1;
+        while (gc < m4 && gc < kThreads) gc <<= 1;
+        const int64_t vc = (m4 + gc - 1) / gc;
+        if (stream_v_ok(3, (int)vc, P.RT)) {
+          L.gc = gc;
+          L.vc = (int)vc;
+          const int NG = kThreads / gc;
+          int64_t rr = std::max<int64_t>(1, target / ((int64_t)NG * L.m));
+          L.trc = (int)(NG * rr);
+          L.fast |= 4u;
+        }
+      }
     } else {
       L.e_off = -1;
       L.ql_off = -1;
@@ -249,6 +281,8 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
       if (mode == 2) bytes += 4.0 * L.r * (double)(2 * L.m + L.n);
     }
     Launch ln;
+    ln.kind = 0;
+    ln.mode = mode;
     ln.seg_off = (int64_t)P.rowsegs.size();
     ln.cb_off = (int64_t)P.ctab.size();
     ln.ncta = split_units(units, min_share, max_grid, P.ctab, [&](const Unit& u, int64_t a, int64_t b) {
@@ -281,6 +315,7 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
       bytes += (ef ? 8.0 : 4.0) * (double)L.n * (double)L.m + 4.0 * L.r * (double)(L.n + 2 * L.m);
     }
     Launch ln;
+    ln.kind = 1;
     ln.seg_off = (int64_t)P.colsegs.size();
     ln.cb_off = (int64_t)P.ctab.size();
     int64_t part = 0;
@@ -323,20 +358,87 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
     ln.bytes = bytes;
     return ln;
   };
+  // TMA stream launch (mode 0: K1 P-step, 2: K3 Q-step, 3: K1 Q-step)
+  auto stream_launch = [&](int mode, const std::vector<int>& tensors) {
+    const uint32_t bit = mode == 0 ? 1u : (mode == 2 ? 2u : 4u);
+    std::vector<Unit> units;
+    double bytes = 0;
+    int64_t stage_floats = 32;
+    for (int i : tensors) {
+      const LayerDesc& L = P.L[i];
+      if (!L.mat) {
+        units.push_back({i, -1, L.n, 8.0, 1024});
+        bytes += 8.0 * L.n;
+        continue;
+      }
+      const double bpe = mode == 0 ? 12.0 : (mode == 2 ? 16.0 : 8.0);
+      const bool fast = (L.fast & bit) != 0;
+      const int64_t tr = fast ? (mode == 3 ? L.trc : L.tr) : 1;
+      if (fast) stage_floats = std::max<int64_t>(stage_floats, tr * L.m);
+      units.push_back({i, -1, L.n, bpe * (double)L.m, tr});
+      bytes += bpe * (double)L.n * (double)L.m;
+      if (mode == 0) bytes += 4.0 * L.r * (double)(L.m + L.n);
+      if (mode == 2) bytes += 4.0 * L.r * (double)(2 * L.m + L.n);
+      if (mode == 3) bytes += 4.0 * L.r * (double)(L.n + 2 * L.m);
+    }
+    Launch ln;
+    ln.kind = 2;
+    ln.mode = mode;
+    ln.seg_off = (int64_t)P.streamsegs.size();
+    ln.cb_off = (int64_t)P.ctab.size();
+    stage_floats = (stage_floats + 31) / 32 * 32;
+    const int64_t budget = 200 * 1024;
+    int stages = (int)std::min<int64_t>(8, budget / (2 * 4 * stage_floats));
+    ln.stages = std::max(2, stages);
+    ln.stage_floats = (int)stage_floats;
+    int64_t part = 0;
+    std::vector<int64_t> first_slot(P.T, -1), nslots(P.T, 0);
+    ln.ncta = split_units(units, min_share, nsm, P.ctab, [&](const Unit& u, int64_t a, int64_t b) {
+      StreamSeg s{};
+      s.layer = u.layer;
+      s.row0 = a;
+      s.row1 = b;
+      const LayerDesc& L = P.L[u.layer];
+      if (mode == 3 && L.mat) {
+        s.nslot = (L.fast & 4u) ? kThreads / L.gc : 1;
+        s.part_off = part;
+        if (first_slot[u.layer] < 0) first_slot[u.layer] = part;
+        s.pidx = (int)nslots[u.layer];
+        nslots[u.layer] += s.nslot;
+        part += (int64_t)s.nslot * L.r * L.m;
+      }
+      P.streamsegs.push_back(s);
+    });
+    for (int64_t k = ln.seg_off; k < (int64_t)P.streamsegs.size(); ++k)
+      P.streamsegs[k].pcount = (int)nslots[P.streamsegs[k].layer];
+    if (mode == 3) P.colpart_elems = std::max(P.colpart_elems, part);
+    ln.bytes = bytes;
+    return ln;
+  };
+  const bool use_stream = P.ef && P.RT <= 8;
+  auto k1_launch = [&](int parity, const std::vector<int>& ts) {
+    if (use_stream) return stream_launch(parity == 0 ? 0 : 3, ts);
+    return parity == 0 ? row_launch(0, ts) : col_launch(ts);
+  };
+  auto k3_launch = [&](int parity, const std::vector<int>& ts) {
+    if (parity == 1 && use_stream) return stream_launch(2, ts);
+    return row_launch(parity == 0 ? 1 : 2, ts);
+  };
   std::vector<int> all(P.T);
   for (int i = 0; i < P.T; ++i) all[i] = i;
-  P.k1_all[0] = row_launch(0, all);
-  P.k3_all[0] = row_launch(1, all);
-  P.k1_all[1] = col_launch(all);
-  P.k3_all[1] = row_launch(2, all);
+  for (int p = 0; p < 2; ++p) {
+    P.k1_all[p] = k1_launch(p, all);
+    P.k3_all[p] = k3_launch(p, all);
+  }
   if (cfg->world_size > 1) {
     for (int p = 0; p < 2; ++p) {
       for (const auto& b : P.buckets[p]) {
-        P.k1_b[p].push_back(p == 0 ? row_launch(0, b) : col_launch(b));
-        P.k3_b[p].push_back(row_launch(p == 0 ? 1 : 2, b));
+        P.k1_b[p].push_back(k1_launch(p, b));
+        P.k3_b[p].push_back(k3_launch(p, b));
       }
     }
   }
+  P.colcnt_n = std::max<int64_t>(P.colcnt_n, P.T);
   // K2 segments per side (0: Q factors, length m; 1: P factors, length n)
   for (int side = 0; side < 2; ++side) {
     int64_t g = 0;
@@ -383,6 +485,7 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
   P.off_grads = take(8 * (size_t)P.T);
   P.off_rowsegs = take(sizeof(RowSeg) * P.rowsegs.size());
   P.off_colsegs = take(sizeof(ColSeg) * P.colsegs.size());
+  P.off_streamsegs = take(sizeof(StreamSeg) * P.streamsegs.size());
   P.off_orth[0] = take(sizeof(OrthSeg) * P.orthsegs[0].size());
   P.off_orth[1] = take(sizeof(OrthSeg) * P.orthsegs[1].size());
   P.off_ctab = take(4 * P.ctab.size());
@@ -465,6 +568,9 @@ const RowSeg* dev_rowsegs(acp_ctx* c, const Launch& ln) {
 const ColSeg* dev_colsegs(acp_ctx* c, const Launch& ln) {
   return reinterpret_cast<const ColSeg*>(c->ws + c->P.off_colsegs) + ln.seg_off;
 }
+const StreamSeg* dev_streamsegs(acp_ctx* c, const Launch& ln) {
+  return reinterpret_cast<const StreamSeg*>(c->ws + c->P.off_streamsegs) + ln.seg_off;
+}
 const int32_t* dev_ctab(acp_ctx* c, const Launch& ln) {
   return reinterpret_cast<const int32_t*>(c->ws + c->P.off_ctab) + ln.cb_off;
 }
@@ -478,7 +584,10 @@ acp_status run_k1(acp_ctx* c, int parity, const Launch& ln, cudaStream_t s) {
   const int ef = c->P.ef ? 1 : 0;
   ProfRec* r = prof_begin(c, parity == 0 ? ACP_K_PROJ_P : ACP_K_PROJ_Q, ln.bytes, s);
   cudaError_t e;
-  if (parity == 0)
+  if (ln.kind == 2)
+    e = launch_stream(ln.mode, c->P.RT, c->tab, dev_streamsegs(c, ln), dev_ctab(c, ln), ln.ncta,
+                      1.0f, ln.stages, ln.stage_floats, s);
+  else if (parity == 0)
     e = launch_row(0, c->P.RT, c->tab, dev_rowsegs(c, ln), dev_ctab(c, ln), ln.ncta, 1.0f, ef, s);
   else
     e = launch_col(c->P.RT, c->tab, dev_colsegs(c, ln), dev_ctab(c, ln), ln.ncta, ef, s);
@@ -492,8 +601,12 @@ acp_status run_k3(acp_ctx* c, int parity, const Launch& ln, cudaStream_t s) {
   if (ln.ncta <= 0) return ACP_OK;
   const int ef = c->P.ef ? 1 : 0;
   ProfRec* r = prof_begin(c, parity == 0 ? ACP_K_DECODE_P : ACP_K_DECODE_Q, ln.bytes, s);
-  cudaError_t e = launch_row(parity == 0 ? 1 : 2, c->P.RT, c->tab, dev_rowsegs(c, ln),
-                             dev_ctab(c, ln), ln.ncta, decode_scale(c), ef, s);
+  cudaError_t e =
+      ln.kind == 2
+          ? launch_stream(ln.mode, c->P.RT, c->tab, dev_streamsegs(c, ln), dev_ctab(c, ln), ln.ncta,
+                          decode_scale(c), ln.stages, ln.stage_floats, s)
+          : launch_row(parity == 0 ? 1 : 2, c->P.RT, c->tab, dev_rowsegs(c, ln), dev_ctab(c, ln),
+                       ln.ncta, decode_scale(c), ef, s);
   prof_end(r, s);
   if (e != cudaSuccess) return cuda_fail(c, e, "decode kernel launch");
   ++c->launches;
@@ -615,6 +728,7 @@ acp_status acp_create(const acp_config* cfg, acp_ctx** out) {
   if ((e = up(P.off_layers, P.L.data(), sizeof(LayerDesc) * P.L.size())) != cudaSuccess ||
       (e = up(P.off_rowsegs, P.rowsegs.data(), sizeof(RowSeg) * P.rowsegs.size())) != cudaSuccess ||
       (e = up(P.off_colsegs, P.colsegs.data(), sizeof(ColSeg) * P.colsegs.size())) != cudaSuccess ||
+      (e = up(P.off_streamsegs, P.streamsegs.data(), sizeof(StreamSeg) * P.streamsegs.size())) != cudaSuccess ||
       (e = up(P.off_orth[0], P.orthsegs[0].data(), sizeof(OrthSeg) * P.orthsegs[0].size())) != cudaSuccess ||
       (e = up(P.off_orth[1], P.orthsegs[1].data(), sizeof(OrthSeg) * P.orthsegs[1].size())) != cudaSuccess ||
       (e = up(P.off_ctab, P.ctab.data(), 4 * P.ctab.size())) != cudaSuccess)

@@ -168,3 +168,28 @@ def test_orthonormal_factor_and_linearity_on_gpu():
     ref = S @ Q @ Q.T / 3
     err = np.linalg.norm(gpu[0]["decoded"][0][0] - ref) / np.linalg.norm(ref)
     assert err < TOL
+
+
+def test_unaligned_gradients_take_generic_path():
+    """Gradient pointers that are not 16-byte aligned cannot use the bulk
+    (TMA) path; the same launch falls back to the generic path per layer."""
+    import torch
+    from paper_2306_08881_b200 import AcpContext
+    from oracle import AcpOracle, rel_frobenius
+    shapes = [(96, 128), (64,), (40, 256)]
+    q0 = make_q0(shapes, 4, SEED)
+    ctx = AcpContext(shapes, 4, seed=SEED, q0=q0)
+    o = AcpOracle(shapes, 4, seed=SEED, q0=q0)
+    for t in range(4):
+        g = [np.random.default_rng([t, i]).standard_normal(s).astype(np.float32) for i, s in enumerate(shapes)]
+        views = []
+        for x in g:
+            base = torch.empty(x.size + 1, device="cuda")
+            v = base[1:].view(x.shape)          # 4-byte offset: not 16-byte aligned
+            v.copy_(torch.from_numpy(x))
+            views.append(v)
+        ctx.step(views, t % 2)
+        ref = o.step([g], t % 2)
+        for a, b in zip(views, ref):
+            assert rel_frobenius(a.cpu().numpy(), b) < TOL
+    ctx.close()
