@@ -11,6 +11,17 @@ constexpr int kMaxV = 8;               // row kernel: float4 chunks per thread p
 constexpr int kOrthRowsPerSeg = 1024;  // K2 work unit (factor rows)
 constexpr int kOrthChunk = 64;         // K2 smem staging (rows)
 
+// Thread mapping of a matrix layer onto a TMA stream kernel CTA (NW warps):
+// a row is covered by `gw` warps (lg = 32) or by `lg` lanes of one warp
+// (gw = 1, 32/lg rows per warp); lane li of the row group owns float4 column
+// chunks c = sub*lg*nc + li + lg*i, i < nc (sub = warp index within the row
+// group). A tile holds tr = (NW/gw)*(32/lg)*rs rows (rs rows per row slot,
+// processed one after another). tr == 0: the layer takes the generic path.
+struct StreamMap {
+  int32_t tr;
+  int16_t lg, gw, nc, rs;
+};
+
 // Per-tensor descriptor uploaded once (device copy of the plan).
 struct LayerDesc {
   int64_t n, m;        // matrix n x m; vector: n = length, m = 0
@@ -26,11 +37,8 @@ struct LayerDesc {
   int32_t pw;          // col kernel: panel width in columns (= 256 * W)
   int64_t w_off;       // K2: offset (doubles) of this layer's two r x r W matrices
   int32_t deg_idx;     // K2: index into the degenerate-mask / counter arrays
-  uint32_t fast;       // stream kernels: bulk-path eligibility (bit0 K1-P, bit1 K3-Q, bit2 K1-Q)
-  int32_t tr;          // stream row kernels: tile rows (multiple of 256 / G)
-  int32_t gc;          // stream col kernel: threads per row
-  int32_t vc;          // stream col kernel: float4 chunks per thread per row
-  int32_t trc;         // stream col kernel: tile rows
+  int32_t pad_;
+  StreamMap sm[3];     // stream kernels: [0] K1 P-step, [1] K3 Q-step, [2] K1 Q-step
 };
 
 // Stream-kernel work unit: rows [row0, row1) of matrix `layer` (or elements of
@@ -111,7 +119,8 @@ cudaError_t launch_col(int rt, const Tables& t, const ColSeg* segs, const int32_
 cudaError_t launch_stream(int mode, int rt, const Tables& t, const StreamSeg* segs,
                           const int32_t* cta_begin, int ncta, float scale, int stages,
                           int stage_floats, cudaStream_t stream);
-bool stream_v_ok(int mode, int V, int rt);
+bool stream_make_map(int mode, int64_t m, int rt, StreamMap* out);
+int stream_ctas_per_sm(int mode);
 size_t stream_smem_bytes(int stages, int stage_floats);
 // K2: CholeskyQR2 of the factors named by segs (side 0: Q factors in the
 // Q-buffer, length m; side 1: P factors in the P-buffer, length n).

@@ -188,32 +188,11 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
       }
       L.W = (L.m % 4 == 0 && P.RT <= 8) ? 4 : ((L.m % 2 == 0 && P.RT <= 16) ? 2 : 1);
       L.pw = kThreads * L.W;
-      // TMA stream kernels: tiles of whole rows (one bulk copy per tensor)
-      L.fast = 0;
-      L.tr = L.trc = 0;
-      L.gc = L.vc = 0;
-      if (P.RT <= 8 && L.m % 4 == 0) {
-        const int64_t m4 = L.m / 4;
-        const int64_t target = 4096;  // floats per tile per tensor (16 KB)
-        if (L.G > 0 && L.V <= 5) {
-          const int NG = kThreads / L.G;
-          int64_t rr = std::max<int64_t>(1, target / ((int64_t)NG * L.m));
-          L.tr = (int)(NG * rr);
-          if (stream_v_ok(0, L.V, P.RT)) L.fast |= 1u;
-          if (stream_v_ok(2, L.V, P.RT)) L.fast |= 2u;
-        }
-        // column kernel prefers one row per 256 threads (one partial slot)
-        int gc = 1;
-        while (gc < m4 && gc < kThreads) gc <<= 1;
-        const int64_t vc = (m4 + gc - 1) / gc;
-        if (stream_v_ok(3, (int)vc, P.RT)) {
-          L.gc = gc;
-          L.vc = (int)vc;
-          const int NG = kThreads / gc;
-          int64_t rr = std::max<int64_t>(1, target / ((int64_t)NG * L.m));
-          L.trc = (int)(NG * rr);
-          L.fast |= 4u;
-        }
+      // TMA stream kernels: thread mapping per mode (tr == 0: generic path)
+      if (P.ef) {
+        stream_make_map(0, L.m, P.RT, &L.sm[0]);
+        stream_make_map(2, L.m, P.RT, &L.sm[1]);
+        stream_make_map(3, L.m, P.RT, &L.sm[2]);
       }
     } else {
       L.e_off = -1;
@@ -360,7 +339,7 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
   };
   // TMA stream launch (mode 0: K1 P-step, 2: K3 Q-step, 3: K1 Q-step)
   auto stream_launch = [&](int mode, const std::vector<int>& tensors) {
-    const uint32_t bit = mode == 0 ? 1u : (mode == 2 ? 2u : 4u);
+    const int mi = mode == 0 ? 0 : (mode == 2 ? 1 : 2);
     std::vector<Unit> units;
     double bytes = 0;
     int64_t stage_floats = 32;
@@ -372,8 +351,8 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
         continue;
       }
       const double bpe = mode == 0 ? 12.0 : (mode == 2 ? 16.0 : 8.0);
-      const bool fast = (L.fast & bit) != 0;
-      const int64_t tr = fast ? (mode == 3 ? L.trc : L.tr) : 1;
+      const bool fast = L.sm[mi].tr > 0;
+      const int64_t tr = fast ? L.sm[mi].tr : 1;
       if (fast) stage_floats = std::max<int64_t>(stage_floats, tr * L.m);
       units.push_back({i, -1, L.n, bpe * (double)L.m, tr});
       bytes += bpe * (double)L.n * (double)L.m;
@@ -387,25 +366,27 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
     ln.seg_off = (int64_t)P.streamsegs.size();
     ln.cb_off = (int64_t)P.ctab.size();
     stage_floats = (stage_floats + 31) / 32 * 32;
-    const int64_t budget = 200 * 1024;
+    const int cps = stream_ctas_per_sm(mode);
+    const int64_t budget = (cps == 1 ? 200 : 96) * 1024;
     int stages = (int)std::min<int64_t>(8, budget / (2 * 4 * stage_floats));
     ln.stages = std::max(2, stages);
     ln.stage_floats = (int)stage_floats;
     int64_t part = 0;
     std::vector<int64_t> first_slot(P.T, -1), nslots(P.T, 0);
-    ln.ncta = split_units(units, min_share, nsm, P.ctab, [&](const Unit& u, int64_t a, int64_t b) {
+    ln.ncta = split_units(units, min_share, nsm * cps, P.ctab, [&](const Unit& u, int64_t a, int64_t b) {
       StreamSeg s{};
       s.layer = u.layer;
       s.row0 = a;
       s.row1 = b;
       const LayerDesc& L = P.L[u.layer];
       if (mode == 3 && L.mat) {
-        s.nslot = (L.fast & 4u) ? kThreads / L.gc : 1;
+        const StreamMap& mp = L.sm[2];
+        s.nslot = mp.tr > 0 ? (mp.tr / mp.rs) : 1;  // row slots of the mapping
         s.part_off = part;
         if (first_slot[u.layer] < 0) first_slot[u.layer] = part;
         s.pidx = (int)nslots[u.layer];
         nslots[u.layer] += s.nslot;
-        part += (int64_t)s.nslot * L.r * L.m;
+        part += (int64_t)s.nslot * round4((int64_t)L.r * L.m);
       }
       P.streamsegs.push_back(s);
     });

@@ -4,29 +4,45 @@
 //   mode 2  K3, Q-step:     E = M' - P Q_loc^T, grad = P Q_agg^T / p
 //   mode 3  K1, Q-step:            Q_loc = M'^T P  (column reduction)
 //
-// with M' = M + E. One producer warp streams contiguous row tiles of M and E
-// (row-major, so a tile of TR rows is ONE cp.async.bulk of TR*m*4 bytes per
-// tensor -> SASS UBLKCP) into an S-stage shared-memory ring guarded by
-// mbarriers (full: TMA complete_tx; empty: one arrive per consumer warp).
-// Eight consumer warps read the tile from shared memory (128-bit, conflict
-// free), keep the layer's orthonormal r-column factor(s) in REGISTERS for the
-// whole segment (thread l owns float4 column chunks c = l + v*G, v < V), and
-// write E / grad back with streaming 128-bit stores. A consumer warp releases
-// its stage as soon as it has pulled the tile into registers, so the producer
-// keeps ~S*2*16 KB of loads in flight per SM independent of compute.
+// with M' = M + E. Thread 0 of the CTA doubles as the producer: it streams
+// contiguous row tiles of M and E (row-major, so a tile of tr rows is ONE
+// cp.async.bulk of tr*m*4 bytes per tensor, SASS UBLKCP) into an S-stage
+// shared-memory ring guarded by mbarriers (full: TMA complete_tx; empty: one
+// arrive per warp), keeping up to S tiles in flight. All NW warps compute:
+// each pulls its slice of the tile from shared memory into registers
+// (128-bit, conflict-free), releases the stage at once, and then works from
+// registers, with the layer's r-column factor(s) also held in registers for
+// the whole segment. Outputs (E, grad) leave with streaming 128-bit stores.
+// A row is covered either by a sub-warp lane group (small m) or by gw whole
+// warps (large m; row sums combined through shared memory behind a named
+// barrier of the row group), so each lane holds at most a few float4 chunks
+// and the code stays branch-free (StreamMap in acp_internal.h).
 //
-// Layers that cannot take the bulk path (m % 4 != 0, m > 5120, gradient not
-// 16-byte aligned, too many factor registers) run a generic consumer-only
-// path in the same launch; vectors (1-D params) are packed/unpacked here too.
+// Layers that cannot take the bulk path (m % 4 != 0, m too large for the
+// register budget, gradient not 16-byte aligned) run a generic path in the
+// same launch; vectors (1-D params) are packed/unpacked here too.
+#include <algorithm>
+
 #include "k_common.cuh"
 
 namespace acp {
 namespace {
 
-constexpr int kCons = 256;                  // consumer threads (all of the CTA)
-constexpr int kConsWarps = kCons / 32;
-constexpr int kStreamThreads = kCons;       // thread 0 doubles as the TMA producer
-constexpr int kRedSlots = 64;
+// NW consumer warps + 1 producer warp per CTA, CPS CTAs per SM (9 warps ->
+// at most 3 per SM sub-partition -> 168 registers per thread), TT = tile
+// target (floats per tensor per stage).
+template <int MODE>
+struct Cfg;
+// K1 P-step: factor in registers (nc*RT float4)
+template <> struct Cfg<0> { static constexpr int NW = 8, CPS = 1, TT = 8192; };
+// K3 Q-step: two factors in registers (2*nc*RT float4), no barriers
+template <> struct Cfg<2> { static constexpr int NW = 8, CPS = 1, TT = 4096; };
+// K1 Q-step: accumulators nc*RT float4 in registers
+template <> struct Cfg<3> { static constexpr int NW = 8, CPS = 1, TT = 8192; };
+
+__host__ __device__ constexpr int nc_max(int mode, int RT) {
+  return mode == 2 ? (RT <= 4 ? 3 : 1) : (RT <= 4 ? 4 : (RT == 8 ? 2 : 0));
+}
 
 __device__ __forceinline__ uint32_t s32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -78,207 +94,153 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(s32(bar)), "l"(policy)
       : "memory");
 }
-__device__ __forceinline__ void cons_sync() {
-  asm volatile("bar.sync 1, %0;" ::"n"(kCons) : "memory");
+template <int NT>
+__device__ __forceinline__ void cta_sync1() {
+  asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+}
+__device__ __forceinline__ void group_bar(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 __device__ __forceinline__ float4 lds4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ float4 zero4() { return make_float4(0.f, 0.f, 0.f, 0.f); }
 
 struct Shared {
   float* sM;
   float* sE;
   uint64_t* full;
   uint64_t* empty;
-  float* red;    // [2][8][kRedSlots]
+  float* red;    // [2][16 warps][8] row-group partial sums
+  float* gred;   // generic path block reduction [16][32]
   int* flag;
   int stage_floats;
   int stages;
 };
 
-// Tile sequence of one CTA: q-th bulk tile uses stage q % S, use (q / S).
-// Consumers keep `q`; thread 0 additionally runs the producer cursor and
-// keeps up to S tiles in flight ahead of the consumers (no dedicated producer
-// warp, so the 8 compute warps keep the full 255-register budget).
+// Consumer position in the tile ring (stage, phase parity).
 struct Pipe {
-  int64_t q = 0;          // next tile to consume
-  // producer state (thread 0)
-  int64_t issued = 0;     // tiles issued so far
-  int psi = 0;            // producer segment cursor
-  int64_t pr0 = -1;       // producer row cursor within segment psi
+  int stage = 0;
+  uint32_t phase = 0;
+  __device__ __forceinline__ void advance(int stages) {
+    if (++stage == stages) {
+      stage = 0;
+      phase ^= 1u;
+    }
+  }
 };
 
 template <int MODE>
-__device__ __forceinline__ bool prod_peek(const Tables& t, const StreamSeg* segs, int se, Pipe& pp,
-                                          const float** src_m, const float** src_e, uint32_t* bytes,
-                                          int64_t* next_r0) {
-  constexpr uint32_t kBit = MODE == 0 ? 1u : (MODE == 2 ? 2u : 4u);
-  while (pp.psi < se) {
-    const StreamSeg& s = segs[pp.psi];
+struct ModeIdx { static constexpr int v = MODE == 0 ? 0 : (MODE == 2 ? 1 : 2); };
+
+template <int MODE>
+__device__ __forceinline__ bool is_fast(const LayerDesc& L, const float* grad) {
+  return L.mat && L.sm[ModeIdx<MODE>::v].tr > 0 && ((reinterpret_cast<uintptr_t>(grad) & 15u) == 0);
+}
+
+// Producer warp (lane 0): walk the CTA's segments and issue every bulk tile
+// as soon as its ring stage is released by all consumer warps.
+template <int MODE>
+__device__ void producer(const Tables& t, const StreamSeg* segs, int sb, int se, const Shared& sh) {
+  const uint64_t pol = policy_evict_first();
+  int stage = 0;
+  uint32_t phase = 0;
+  for (int si = sb; si < se; ++si) {
+    const StreamSeg s = segs[si];
     const LayerDesc& L = t.layers[s.layer];
     const float* grad = t.grads[s.layer];
-    const bool fast = L.mat && (L.fast & kBit) && ((reinterpret_cast<uintptr_t>(grad) & 15u) == 0);
-    if (pp.pr0 < 0) pp.pr0 = s.row0;
-    if (!fast || pp.pr0 >= s.row1) {
-      ++pp.psi;
-      pp.pr0 = -1;
-      continue;
-    }
-    const int TR = MODE == 3 ? L.trc : L.tr;
-    const int64_t nr = (s.row1 - pp.pr0) < TR ? (s.row1 - pp.pr0) : TR;
-    *src_m = grad + pp.pr0 * L.m;
-    *src_e = t.E + L.e_off + pp.pr0 * L.m;
-    *bytes = (uint32_t)(nr * L.m * 4);
-    *next_r0 = pp.pr0 + TR;
-    return true;
-  }
-  return false;
-}
-
-// Called by thread 0 before consuming tile pp.q: makes sure tile q has been
-// issued (blocking on its stage if needed) and opportunistically issues the
-// following tiles whose stages are already free.
-template <int MODE>
-__device__ void prod_pump(const Tables& t, const StreamSeg* segs, int se, Pipe& pp,
-                          const Shared& sh, uint64_t pol) {
-  while (pp.issued < pp.q + sh.stages) {
-    const int stage = (int)(pp.issued % sh.stages);
-    const float *sm_src, *se_src;
-    uint32_t bytes;
-    int64_t nr0;
-    if (!prod_peek<MODE>(t, segs, se, pp, &sm_src, &se_src, &bytes, &nr0)) break;
-    if (pp.issued >= sh.stages) {
-      const uint32_t par = (uint32_t)(((pp.issued / sh.stages) - 1) & 1);
-      if (pp.issued == pp.q) mbar_wait(&sh.empty[stage], par);
-      else if (!mbar_test(&sh.empty[stage], par)) break;
-    }
-    mbar_arrive_tx(&sh.full[stage], 2 * bytes);
-    bulk_g2s(sh.sM + (size_t)stage * sh.stage_floats, sm_src, bytes, &sh.full[stage], pol);
-    bulk_g2s(sh.sE + (size_t)stage * sh.stage_floats, se_src, bytes, &sh.full[stage], pol);
-    pp.pr0 = nr0;
-    ++pp.issued;
-  }
-}
-
-// Group sum over G threads (G | 256); every thread of the group gets the sums.
-template <int N>
-__device__ __forceinline__ void group_sum(float (&a)[N], int G, float* red, int& rph) {
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    if (off < G) {
-#pragma unroll
-      for (int i = 0; i < N; ++i) a[i] += __shfl_xor_sync(0xffffffffu, a[i], off);
-    }
-  }
-  if (G <= 32) return;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  float* buf = red + (rph & 1) * (kConsWarps * kRedSlots);
-  ++rph;
-#pragma unroll
-  for (int i = 0; i < N; ++i)
-    if (lane == (i & 31)) buf[warp * kRedSlots + i] = a[i];
-  cons_sync();
-  const int nw = G >> 5;
-  const int w0 = (warp / nw) * nw;
-#pragma unroll
-  for (int i = 0; i < N; ++i) {
-    float s = buf[w0 * kRedSlots + i];
-    for (int w = 1; w < nw; ++w) s += buf[(w0 + w) * kRedSlots + i];
-    a[i] = s;
-  }
-}
-
-template <int RT>
-__device__ __forceinline__ void block_sum_cons(float (&a)[RT], float* red) {
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-#pragma unroll
-    for (int k = 0; k < RT; ++k) a[k] += __shfl_xor_sync(0xffffffffu, a[k], off);
-  }
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  cons_sync();
-#pragma unroll
-  for (int k = 0; k < RT; ++k)
-    if (lane == (k & 31)) red[warp * 32 + k] = a[k];
-  cons_sync();
-#pragma unroll
-  for (int k = 0; k < RT; ++k) {
-    float s = red[k];
-    for (int w = 1; w < kConsWarps; ++w) s += red[w * 32 + k];
-    a[k] = s;
-  }
-}
-
-__host__ __device__ constexpr bool v_ok(int mode, int V, int RT) {
-  return mode == 0 ? V * RT <= 24 : (mode == 2 ? 2 * V * RT <= 40 : V * RT <= 24);
-}
-
-// ---------------------------------------------------------------------------
-// fast (bulk-pipelined) segment, consumer side
-// ---------------------------------------------------------------------------
-template <int MODE, int RT, int V>
-__device__ void seg_fast(const Tables& t, const LayerDesc& L, const StreamSeg& s,
-                         float* __restrict__ grad, float scale, const Shared& sh, Pipe& pp,
-                         int& rph, const StreamSeg* segs, int se, uint64_t pol) {
-  const int G = MODE == 3 ? L.gc : L.G;
-  const int TR = MODE == 3 ? L.trc : L.tr;
-  const int NG = kCons / G;
-  const int RR = TR / NG;
-  const int g = threadIdx.x / G, l = threadIdx.x - g * G;
-  const int lane = threadIdx.x & 31;
-  const int64_t m = L.m, n = L.n;
-  const int m4 = (int)(m >> 2);
-  const int r = L.r;
-  float* __restrict__ E = t.E + L.e_off;
-
-  // factor(s) in registers for the whole segment
-  float4 qa[V][RT];   // mode 0: Q (orthonormal); mode 2: Q_agg
-  float4 qb[MODE == 2 ? V : 1][MODE == 2 ? RT : 1];  // mode 2: Q_loc
-  float4 acc3[MODE == 3 ? V : 1][MODE == 3 ? RT : 1];
-  if constexpr (MODE == 0 || MODE == 2) {
-    const float* Qf = t.qbuf + L.q_off;
-#pragma unroll
-    for (int v = 0; v < V; ++v) {
-      const int c = l + v * G;
-#pragma unroll
-      for (int k = 0; k < RT; ++k) {
-        qa[v][k] = (c < m4 && k < r) ? ld_f4(Qf + k * m + 4 * c) : make_float4(0.f, 0.f, 0.f, 0.f);
-        if constexpr (MODE == 2)
-          qb[v][k] = (c < m4 && k < r) ? ld_f4(t.qloc + L.ql_off + k * m + 4 * c)
-                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+    if (!is_fast<MODE>(L, grad)) continue;
+    const int64_t m = L.m;
+    const int tr = L.sm[ModeIdx<MODE>::v].tr;
+    const float* pm = grad + s.row0 * m;
+    const float* pe = t.E + L.e_off + s.row0 * m;
+    for (int64_t r0 = s.row0; r0 < s.row1; r0 += tr) {
+      const int64_t nr = (s.row1 - r0) < tr ? (s.row1 - r0) : tr;
+      const uint32_t bytes = (uint32_t)(nr * m * 4);
+      mbar_wait(&sh.empty[stage], phase ^ 1u);
+      mbar_arrive_tx(&sh.full[stage], 2 * bytes);
+      bulk_g2s(sh.sM + (size_t)stage * sh.stage_floats, pm, bytes, &sh.full[stage], pol);
+      bulk_g2s(sh.sE + (size_t)stage * sh.stage_floats, pe, bytes, &sh.full[stage], pol);
+      pm += nr * m;
+      pe += nr * m;
+      if (++stage == sh.stages) {
+        stage = 0;
+        phase ^= 1u;
       }
     }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// fast (bulk-pipelined) segment
+// ---------------------------------------------------------------------------
+template <int MODE, int RT, int NC>
+__device__ void seg_fast(const Tables& t, const LayerDesc& L, const StreamSeg& s,
+                         float* __restrict__ grad, float scale, const Shared& sh, Pipe& pp,
+                         int& rph) {
+  constexpr int NW = Cfg<MODE>::NW;
+  const StreamMap mp = L.sm[ModeIdx<MODE>::v];
+  const int lg = mp.lg, gw = mp.gw, rs = mp.rs, TR = mp.tr;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int sub = warp % gw, wrow = warp / gw;
+  const int lgi = lane / lg, li = lane - lgi * lg;
+  const int rowslot = wrow * (32 / lg) + lgi;
+  const int NRS = (NW / gw) * (32 / lg);
+  const int m = (int)L.m;
+  const int n = (int)L.n;
+  const int m4 = m >> 2;
+  const int r = L.r;
+  const int cbase = sub * lg * NC + li;
+  int coff[NC];
+  bool cval[NC];
+#pragma unroll
+  for (int i = 0; i < NC; ++i) {
+    const int c = cbase + lg * i;
+    cval[i] = c < m4;
+    coff[i] = 4 * (cval[i] ? c : 0);
+  }
+  float* __restrict__ E = t.E + L.e_off;
+  const float* __restrict__ Pf = t.pbuf + L.p_off;  // k-major [r][n]
+
+  // factor(s) in registers for the whole segment (k >= r and invalid chunks: 0)
+  float4 qa[MODE == 3 ? 1 : NC][MODE == 3 ? 1 : RT];
+  float4 qb[MODE == 2 ? NC : 1][MODE == 2 ? RT : 1];
+  float4 acc3[MODE == 3 ? NC : 1][MODE == 3 ? RT : 1];
+  if constexpr (MODE != 3) {
+    const float* Qf = t.qbuf + L.q_off;
+    const float* Ql = t.qloc + L.ql_off;
+#pragma unroll
+    for (int i = 0; i < NC; ++i)
+#pragma unroll
+      for (int k = 0; k < RT; ++k) {
+        const bool ok = cval[i] && k < r;
+        qa[i][k] = ok ? ld_f4(Qf + k * m + coff[i]) : zero4();
+        if constexpr (MODE == 2) qb[i][k] = ok ? ld_f4(Ql + k * m + coff[i]) : zero4();
+      }
   } else {
 #pragma unroll
-    for (int v = 0; v < V; ++v)
+    for (int i = 0; i < NC; ++i)
 #pragma unroll
-      for (int k = 0; k < RT; ++k) acc3[v][k] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int k = 0; k < RT; ++k) acc3[i][k] = zero4();
   }
-  const float* __restrict__ Pf = t.pbuf + L.p_off;  // k-major [r][n]
-  float* __restrict__ Pw = t.pbuf + L.p_off;
 
   for (int64_t r0 = s.row0; r0 < s.row1; r0 += TR) {
     const int nr = (int)((s.row1 - r0) < TR ? (s.row1 - r0) : TR);
-    if (threadIdx.x == 0) prod_pump<MODE>(t, segs, se, pp, sh, pol);
-    const int stage = (int)(pp.q % sh.stages);
-    mbar_wait(&sh.full[stage], (uint32_t)((pp.q / sh.stages) & 1));
+    const int stage = pp.stage;
+    mbar_wait(&sh.full[stage], pp.phase);
     const float* tM = sh.sM + (size_t)stage * sh.stage_floats;
     const float* tE = sh.sE + (size_t)stage * sh.stage_floats;
-    for (int j = 0; j < RR; ++j) {
-      const int li = g + NG * j;
-      const bool valid = li < nr;
-      const int64_t row = r0 + li;
-      float pk[RT];
-      if constexpr (MODE != 0) {
+    for (int j = 0; j < rs; ++j) {
+      const int tri = rowslot + NRS * j;  // row within the tile
+      const bool rval = tri < nr;
+      const int64_t row = r0 + (rval ? tri : 0);
+      const int toff = (rval ? tri : 0) * m;
+      float4 x[NC];
 #pragma unroll
-        for (int k = 0; k < RT; ++k) pk[k] = (valid && k < r) ? __ldg(Pf + k * n + row) : 0.f;
+      for (int i = 0; i < NC; ++i) {
+        const float4 a = lds4(tM + toff + coff[i]);
+        const float4 b = lds4(tE + toff + coff[i]);
+        x[i] = (rval && cval[i]) ? f4add(a, b) : zero4();
       }
-      float4 x[V];
-#pragma unroll
-      for (int v = 0; v < V; ++v) {
-        const int c = l + v * G;
-        x[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (valid && c < m4) x[v] = f4add(lds4(tM + li * m + 4 * c), lds4(tE + li * m + 4 * c));
-      }
-      if (j == RR - 1) {
+      if (j == rs - 1) {
         __syncwarp();
         if (lane == 0) mbar_arrive(&sh.empty[stage]);
       }
@@ -288,79 +250,139 @@ __device__ void seg_fast(const Tables& t, const LayerDesc& L, const StreamSeg& s
         for (int k = 0; k < RT; ++k) {
           float a = 0.f;
 #pragma unroll
-          for (int v = 0; v < V; ++v) a += f4dot(x[v], qa[v][k]);
+          for (int i = 0; i < NC; ++i) a += f4dot(x[i], qa[i][k]);
           acc[k] = a;
         }
-        group_sum<RT>(acc, G, sh.red, rph);
-        if (valid) {
+        // sum over the lg lanes of the row group (butterfly: all lanes get it)
 #pragma unroll
-          for (int v = 0; v < V; ++v) {
-            const int c = l + v * G;
-            if (c < m4) {
-              float4 e = x[v];
+        for (int off = 16; off > 0; off >>= 1) {
+          if (off < lg) {
 #pragma unroll
-              for (int k = 0; k < RT; ++k) f4fma(e, -acc[k], qa[v][k]);
-              st_cs4(E + row * m + 4 * c, e);
-            }
-          }
-          if (l == 0) {
-#pragma unroll
-            for (int k = 0; k < RT; ++k)
-              if (k < r) Pw[k * n + row] = acc[k];
+            for (int k = 0; k < RT; ++k) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], off);
           }
         }
-      } else if constexpr (MODE == 2) {
-        if (valid) {
+        // ... and over the gw warps of the row group (shared memory). The
+        // barrier spans the whole CTA: named barriers with per-group thread
+        // counts could alias across consecutive segments with different gw.
+        if (gw > 1) {
+          float* buf = sh.red + (rph & 1) * (16 * 8);  // [2][16 warps][8]
+          if (lane < RT) {
+            float v = acc[0];
 #pragma unroll
-          for (int v = 0; v < V; ++v) {
-            const int c = l + v * G;
-            if (c < m4) {
-              float4 e = x[v], o = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int k = 1; k < RT; ++k)
+              if (lane == k) v = acc[k];
+            buf[warp * 8 + lane] = v;
+          }
+          cta_sync1<NW * 32>();  // uniform across the CTA (every warp has the same rows)
+          const float* gb = buf + (wrow * gw) * 8;
 #pragma unroll
-              for (int k = 0; k < RT; ++k) {
-                f4fma(e, -pk[k], qb[v][k]);
-                f4fma(o, pk[k], qa[v][k]);
+          for (int k = 0; k < RT; ++k) acc[k] = 0.f;
+          for (int w = 0; w < gw; ++w) {
+            if constexpr (RT >= 4) {
+#pragma unroll
+              for (int k = 0; k < RT; k += 4) {
+                const float4 v = lds4(gb + w * 8 + k);
+                acc[k] += v.x;
+                acc[k + 1] += v.y;
+                acc[k + 2] += v.z;
+                acc[k + 3] += v.w;
               }
-              st_cs4(E + row * m + 4 * c, e);
-              st_cs4(grad + row * m + 4 * c, f4scale(o, scale));
+            } else {
+#pragma unroll
+              for (int k = 0; k < RT; ++k) acc[k] += gb[w * 8 + k];
             }
           }
+        }
+        ++rph;
+#pragma unroll
+        for (int i = 0; i < NC; ++i) {
+          float4 e = x[i];
+#pragma unroll
+          for (int k = 0; k < RT; ++k) f4fma(e, -acc[k], qa[i][k]);
+          if (rval && cval[i]) st_cs4(E + row * m + coff[i], e);
+        }
+        if (rval && sub == 0 && li == 0) {
+#pragma unroll
+          for (int k = 0; k < RT; ++k)
+            if (k < r) t.pbuf[L.p_off + (int64_t)k * n + row] = acc[k];
         }
       } else {
+        float pk[RT];
 #pragma unroll
-        for (int v = 0; v < V; ++v)
+        for (int k = 0; k < RT; ++k) pk[k] = (k < r) ? __ldg(Pf + (int64_t)k * n + row) : 0.f;
+        if constexpr (MODE == 2) {
 #pragma unroll
-          for (int k = 0; k < RT; ++k) {
-            acc3[v][k].x = fmaf(x[v].x, pk[k], acc3[v][k].x);
-            acc3[v][k].y = fmaf(x[v].y, pk[k], acc3[v][k].y);
-            acc3[v][k].z = fmaf(x[v].z, pk[k], acc3[v][k].z);
-            acc3[v][k].w = fmaf(x[v].w, pk[k], acc3[v][k].w);
+          for (int i = 0; i < NC; ++i) {
+            float4 e = x[i], o = zero4();
+#pragma unroll
+            for (int k = 0; k < RT; ++k) {
+              f4fma(e, -pk[k], qb[i][k]);
+              f4fma(o, pk[k], qa[i][k]);
+            }
+            if (rval && cval[i]) {
+              st_cs4(E + row * m + coff[i], e);
+              st_cs4(grad + row * m + coff[i], f4scale(o, scale));
+            }
           }
+        } else {
+#pragma unroll
+          for (int i = 0; i < NC; ++i)
+#pragma unroll
+            for (int k = 0; k < RT; ++k) {
+              acc3[i][k].x = fmaf(x[i].x, pk[k], acc3[i][k].x);
+              acc3[i][k].y = fmaf(x[i].y, pk[k], acc3[i][k].y);
+              acc3[i][k].z = fmaf(x[i].z, pk[k], acc3[i][k].z);
+              acc3[i][k].w = fmaf(x[i].w, pk[k], acc3[i][k].w);
+            }
+        }
       }
     }
-    ++pp.q;
+    pp.advance(sh.stages);
   }
   if constexpr (MODE == 3) {
-    // partial slot g of this segment: k-major [r][m]
-    float* part = t.colpart + s.part_off + (int64_t)g * r * m;
+    // partial slot `rowslot` of this segment: k-major [r][m], 16-byte stride
+    const int64_t stride = ((int64_t)r * m + 3) & ~int64_t(3);
+    float* part = t.colpart + s.part_off + (int64_t)rowslot * stride;
 #pragma unroll
-    for (int v = 0; v < V; ++v) {
-      const int c = l + v * G;
-      if (c < m4) {
+    for (int i = 0; i < NC; ++i) {
+      if (cval[i]) {
 #pragma unroll
         for (int k = 0; k < RT; ++k)
-          if (k < r) *reinterpret_cast<float4*>(part + k * m + 4 * c) = acc3[v][k];
+          if (k < r) *reinterpret_cast<float4*>(part + (int64_t)k * m + coff[i]) = acc3[i][k];
       }
     }
   }
 }
 
 // ---------------------------------------------------------------------------
-// generic segment (any m / alignment), consumer threads only
+// generic segment (any m / alignment)
 // ---------------------------------------------------------------------------
+template <int NT, int RT>
+__device__ __forceinline__ void block_sum(float (&a)[RT], float* red) {
+  constexpr int NWp = NT / 32;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+    for (int k = 0; k < RT; ++k) a[k] += __shfl_xor_sync(0xffffffffu, a[k], off);
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  cta_sync1<NT>();
+#pragma unroll
+  for (int k = 0; k < RT; ++k)
+    if (lane == (k & 31)) red[warp * 32 + k] = a[k];
+  cta_sync1<NT>();
+#pragma unroll
+  for (int k = 0; k < RT; ++k) {
+    float s = red[k];
+    for (int w = 1; w < NWp; ++w) s += red[w * 32 + k];
+    a[k] = s;
+  }
+}
+
 template <int MODE, int RT>
 __device__ void seg_generic(const Tables& t, const LayerDesc& L, const StreamSeg& s,
                             float* __restrict__ grad, float scale, float* red) {
+  constexpr int NT = Cfg<MODE>::NW * 32;
   const int64_t m = L.m, n = L.n;
   const int r = L.r;
   const float* __restrict__ Qs = t.qbuf + L.q_off;
@@ -369,12 +391,13 @@ __device__ void seg_generic(const Tables& t, const LayerDesc& L, const StreamSeg
   float* __restrict__ E = t.E + L.e_off;
   if constexpr (MODE == 3) {
     float* part = t.colpart + s.part_off;
-    for (int64_t c0 = 0; c0 < m; c0 += kCons) {
+    const int64_t stride = ((int64_t)r * m + 3) & ~int64_t(3);
+    for (int64_t c0 = 0; c0 < m; c0 += NT) {
       const int64_t c = c0 + threadIdx.x;
-      float acc[RT];
-#pragma unroll
-      for (int k = 0; k < RT; ++k) acc[k] = 0.f;
       if (c < m) {
+        float acc[RT];
+#pragma unroll
+        for (int k = 0; k < RT; ++k) acc[k] = 0.f;
         for (int64_t row = s.row0; row < s.row1; ++row) {
           const float x = grad[row * m + c] + E[row * m + c];
 #pragma unroll
@@ -385,7 +408,7 @@ __device__ void seg_generic(const Tables& t, const LayerDesc& L, const StreamSeg
         for (int k = 0; k < RT; ++k)
           if (k < r) part[k * m + c] = acc[k];
         for (int gsl = 1; gsl < s.nslot; ++gsl)
-          for (int k = 0; k < r; ++k) part[(int64_t)gsl * r * m + k * m + c] = 0.f;
+          for (int k = 0; k < r; ++k) part[(int64_t)gsl * stride + k * m + c] = 0.f;
       }
     }
     return;
@@ -397,14 +420,14 @@ __device__ void seg_generic(const Tables& t, const LayerDesc& L, const StreamSeg
       float acc[RT];
 #pragma unroll
       for (int k = 0; k < RT; ++k) acc[k] = 0.f;
-      for (int64_t j = threadIdx.x; j < m; j += kCons) {
+      for (int64_t j = threadIdx.x; j < m; j += NT) {
         const float x = gr[j] + er[j];
 #pragma unroll
         for (int k = 0; k < RT; ++k)
           if (k < r) acc[k] = fmaf(x, __ldg(Qs + k * m + j), acc[k]);
       }
-      block_sum_cons<RT>(acc, red);
-      for (int64_t j = threadIdx.x; j < m; j += kCons) {
+      block_sum<NT, RT>(acc, red);
+      for (int64_t j = threadIdx.x; j < m; j += NT) {
         float x = gr[j] + er[j];
 #pragma unroll
         for (int k = 0; k < RT; ++k)
@@ -420,7 +443,7 @@ __device__ void seg_generic(const Tables& t, const LayerDesc& L, const StreamSeg
       float p[RT];
 #pragma unroll
       for (int k = 0; k < RT; ++k) p[k] = (k < r) ? __ldg(Ps + k * n + row) : 0.f;
-      for (int64_t j = threadIdx.x; j < m; j += kCons) {
+      for (int64_t j = threadIdx.x; j < m; j += NT) {
         float x = gr[j] + er[j], o = 0.f;
 #pragma unroll
         for (int k = 0; k < RT; ++k) {
@@ -437,26 +460,27 @@ __device__ void seg_generic(const Tables& t, const LayerDesc& L, const StreamSeg
 }
 
 // last segment of a layer to finish (mode 3): sum the layer's partial slots in
-// slot order into the Q-buffer slot and the local-Q copy
+// slot order into the Q-buffer slot and the local-Q copy (deterministic)
+template <int NT>
 __device__ void col_finish(const Tables& t, const LayerDesc& L, const StreamSeg& s, int* flag) {
   __threadfence();
-  cons_sync();
+  cta_sync1<NT>();
   if (threadIdx.x == 0) {
     const int old = atomicAdd(t.colcnt + s.layer, s.nslot);
     *flag = (old + s.nslot == s.pcount);
   }
-  cons_sync();
+  cta_sync1<NT>();
   if (!*flag) return;
   __threadfence();
   const int64_t m = L.m;
   const int r = L.r;
-  const int64_t slot = (int64_t)r * m;
+  const int64_t slot = ((int64_t)r * m + 3) & ~int64_t(3);
   const float* first = t.colpart + s.part_off - (int64_t)s.pidx * slot;
   float* Qs = t.qbuf + L.q_off;
   float* Ql = t.qloc + L.ql_off;
-  const int64_t total = slot;
+  const int64_t total = (int64_t)r * m;
   if ((m & 3) == 0) {
-    for (int64_t i = 4 * threadIdx.x; i < total; i += 4 * kCons) {
+    for (int64_t i = 4 * threadIdx.x; i < total; i += 4 * NT) {
       float4 acc = __ldcg(reinterpret_cast<const float4*>(first + i));
       for (int p = 1; p < s.pcount; ++p)
         acc = f4add(acc, __ldcg(reinterpret_cast<const float4*>(first + p * slot + i)));
@@ -464,7 +488,7 @@ __device__ void col_finish(const Tables& t, const LayerDesc& L, const StreamSeg&
       *reinterpret_cast<float4*>(Ql + i) = acc;
     }
   } else {
-    for (int64_t i = threadIdx.x; i < total; i += kCons) {
+    for (int64_t i = threadIdx.x; i < total; i += NT) {
       float acc = __ldcg(first + i);
       for (int p = 1; p < s.pcount; ++p) acc += __ldcg(first + p * slot + i);
       Qs[i] = acc;
@@ -475,9 +499,10 @@ __device__ void col_finish(const Tables& t, const LayerDesc& L, const StreamSeg&
 }
 
 template <int MODE, int RT>
-__global__ void __launch_bounds__(kStreamThreads, 1)
+__global__ void __launch_bounds__(Cfg<MODE>::NW * 32 + 32, Cfg<MODE>::CPS)
     stream_kernel(Tables t, const StreamSeg* __restrict__ segs, const int32_t* __restrict__ cta_begin,
                   float scale, int stages, int stage_floats) {
+  constexpr int NT = Cfg<MODE>::NW * 32;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Shared sh;
   sh.stages = stages;
@@ -487,73 +512,70 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
   sh.full = reinterpret_cast<uint64_t*>(sh.sE + (size_t)stages * stage_floats);
   sh.empty = sh.full + stages;
   sh.red = reinterpret_cast<float*>(sh.empty + stages);
-  sh.flag = reinterpret_cast<int*>(sh.red + 2 * kConsWarps * kRedSlots);
+  sh.gred = sh.red + 2 * 16 * 8;
+  sh.flag = reinterpret_cast<int*>(sh.gred + 16 * 32);
   if (threadIdx.x == 0) {
     for (int i = 0; i < stages; ++i) {
       mbar_init(&sh.full[i], 1);
-      mbar_init(&sh.empty[i], kConsWarps);
+      mbar_init(&sh.empty[i], Cfg<MODE>::NW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   const int sb = cta_begin[blockIdx.x], se = cta_begin[blockIdx.x + 1];
-  constexpr uint32_t kBit = MODE == 0 ? 1u : (MODE == 2 ? 2u : 4u);
-
-  const uint64_t pol = policy_evict_first();
-  // ---------------- consumers ----------------
+  if ((threadIdx.x >> 5) == Cfg<MODE>::NW) {  // producer warp
+    if ((threadIdx.x & 31) == 0) producer<MODE>(t, segs, sb, se, sh);
+    return;
+  }
   Pipe pp;
-  pp.psi = sb;
   int rph = 0;
   for (int si = sb; si < se; ++si) {
     const StreamSeg s = segs[si];
-    const LayerDesc L = t.layers[s.layer];
+    const LayerDesc& L = t.layers[s.layer];
     float* grad = t.grads[s.layer];
     if (!L.mat) {
       if (MODE == 0) {
         float* slot = t.pbuf + L.p_off;
-        for (int64_t i = s.row0 + threadIdx.x; i < s.row1; i += kCons) slot[i] = grad[i];
+        for (int64_t i = s.row0 + threadIdx.x; i < s.row1; i += NT) slot[i] = grad[i];
       } else if (MODE == 3) {
         float* slot = t.qbuf + L.q_off;
-        for (int64_t i = s.row0 + threadIdx.x; i < s.row1; i += kCons) slot[i] = grad[i];
+        for (int64_t i = s.row0 + threadIdx.x; i < s.row1; i += NT) slot[i] = grad[i];
       } else {
         const float* slot = t.qbuf + L.q_off;
-        for (int64_t i = s.row0 + threadIdx.x; i < s.row1; i += kCons) grad[i] = slot[i] * scale;
+        for (int64_t i = s.row0 + threadIdx.x; i < s.row1; i += NT) grad[i] = slot[i] * scale;
       }
       continue;
     }
-    const bool fast = (L.fast & kBit) && ((reinterpret_cast<uintptr_t>(grad) & 15u) == 0);
-    if (!fast) {
-      seg_generic<MODE, RT>(t, L, s, grad, scale, sh.red);
+    if (!is_fast<MODE>(L, grad)) {
+      seg_generic<MODE, RT>(t, L, s, grad, scale, sh.gred);
     } else {
-      const int V = MODE == 3 ? L.vc : L.V;
-      switch (V) {
-#define ACP_CASE(VV)                                                       \
-  case VV:                                                                 \
-    if constexpr (v_ok(MODE, VV, RT)) seg_fast<MODE, RT, VV>(t, L, s, grad, scale, sh, pp, rph, segs, se, pol); \
+      switch (L.sm[ModeIdx<MODE>::v].nc) {
+#define ACP_CASE(NCV)                                                            \
+  case NCV:                                                                      \
+    if constexpr (NCV <= nc_max(MODE, RT))                                       \
+      seg_fast<MODE, RT, NCV>(t, L, s, grad, scale, sh, pp, rph);                  \
     break;
         ACP_CASE(1)
         ACP_CASE(2)
         ACP_CASE(3)
         ACP_CASE(4)
-        ACP_CASE(5)
 #undef ACP_CASE
         default: break;
       }
     }
-    if constexpr (MODE == 3) col_finish(t, L, s, sh.flag);
+    if constexpr (MODE == 3) col_finish<NT>(t, L, s, sh.flag);
   }
 }
 
 template <int MODE>
 cudaError_t launch_mode(int rt, const Tables& t, const StreamSeg* segs, const int32_t* cb, int ncta,
                         float scale, int stages, int stage_floats, cudaStream_t st) {
-  const size_t smem = (size_t)2 * stages * stage_floats * 4 + 2 * stages * 8 +
-                      2 * kConsWarps * kRedSlots * 4 + 16;
+  const size_t smem = stream_smem_bytes(stages, stage_floats);
   auto go = [&](auto kern) -> cudaError_t {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
-    kern<<<ncta, kStreamThreads, smem, st>>>(t, segs, cb, scale, stages, stage_floats);
+    kern<<<ncta, Cfg<MODE>::NW * 32 + 32, smem, st>>>(t, segs, cb, scale, stages, stage_floats);
     return cudaGetLastError();
   };
   switch (rt) {
@@ -567,10 +589,50 @@ cudaError_t launch_mode(int rt, const Tables& t, const StreamSeg* segs, const in
 
 }  // namespace
 
-bool stream_v_ok(int mode, int V, int rt) { return V >= 1 && V <= 5 && v_ok(mode, V, rt); }
-
 size_t stream_smem_bytes(int stages, int stage_floats) {
-  return (size_t)2 * stages * stage_floats * 4 + 2 * stages * 8 + 2 * kConsWarps * kRedSlots * 4 + 16;
+  return (size_t)2 * stages * stage_floats * 4 + 2 * stages * 8 + (2 * 16 * 8 + 16 * 32) * 4 + 16;
+}
+
+// Host: choose the thread mapping of an m-column layer for stream mode
+// `mode` (0, 2, 3); returns false (generic path) when it does not fit.
+int stream_ctas_per_sm(int mode) {
+  return mode == 0 ? Cfg<0>::CPS : (mode == 2 ? Cfg<2>::CPS : Cfg<3>::CPS);
+}
+
+bool stream_make_map(int mode, int64_t m, int rt, StreamMap* out) {
+  *out = StreamMap{0, 0, 0, 0, 0};
+  if (m % 4 != 0 || rt > 8) return false;
+  const int NW = mode == 0 ? Cfg<0>::NW : (mode == 2 ? Cfg<2>::NW : Cfg<3>::NW);
+  const int64_t TT = mode == 0 ? Cfg<0>::TT : (mode == 2 ? Cfg<2>::TT : Cfg<3>::TT);
+  const int ncm = nc_max(mode, rt);
+  if (ncm <= 0) return false;
+  const int64_t m4 = m / 4;
+  if (m4 < 32) {  // sub-warp row groups
+    int lg = 1;
+    while (lg < m4) lg <<= 1;
+    const int64_t nrs = (int64_t)NW * (32 / lg);
+    const int64_t rs = std::max<int64_t>(1, TT / (nrs * m));
+    out->lg = (int16_t)lg;
+    out->gw = 1;
+    out->nc = 1;
+    out->rs = (int16_t)rs;
+    out->tr = (int32_t)(nrs * rs);
+    return true;
+  }
+  for (int gw = 1; gw <= NW; gw <<= 1) {
+    const int64_t nc = (m4 + 32LL * gw - 1) / (32LL * gw);
+    if (nc > ncm) continue;
+    const int64_t nrs = NW / gw;
+    if (gw < NW && nrs * m > TT) continue;  // tile would exceed the target
+    const int64_t rs = std::max<int64_t>(1, TT / (nrs * m));
+    out->lg = 32;
+    out->gw = (int16_t)gw;
+    out->nc = (int16_t)nc;
+    out->rs = (int16_t)rs;
+    out->tr = (int32_t)(nrs * rs);
+    return true;
+  }
+  return false;
 }
 
 cudaError_t launch_stream(int mode, int rt, const Tables& t, const StreamSeg* segs,
