@@ -17,9 +17,14 @@ constexpr int kOrthChunk = 64;         // K2 smem staging (rows)
 // chunks c = sub*lg*nc + li + lg*i, i < nc (sub = warp index within the row
 // group). A tile holds tr = (NW/gw)*(32/lg)*rs rows (rs rows per row slot,
 // processed one after another). tr == 0: the layer takes the generic path.
+// Column panels (modes 2, 3 only): the row is split into np panels of pcols
+// columns (the last one narrower); each panel is a separate work unit, so the
+// per-thread factor registers stay bounded for wide layers.
 struct StreamMap {
   int32_t tr;
   int16_t lg, gw, nc, rs;
+  int32_t pcols;
+  int16_t np, pad_;
 };
 
 // Per-tensor descriptor uploaded once (device copy of the plan).
@@ -44,7 +49,8 @@ struct LayerDesc {
 // Stream-kernel work unit: rows [row0, row1) of matrix `layer` (or elements of
 // a vector). Column mode: the segment writes `nslot` partial slots (r x m
 // floats each, k-major) starting at part_off; the layer's `pcount` slots are
-// contiguous and slot index of this segment's first one is `pidx`.
+// contiguous and slot index of this segment's first one is `pidx`. Slots are
+// r x pcols floats (k-major), stride round4(r * pcols).
 struct StreamSeg {
   int32_t layer;
   int32_t nslot;
@@ -52,6 +58,8 @@ struct StreamSeg {
   int64_t part_off;
   int32_t pidx;
   int32_t pcount;
+  int32_t panel;     // column panel (modes 2, 3)
+  int32_t counter;   // mode 3: completion counter of (layer, panel)
 };
 
 // Row-kernel work unit: rows [row0, row1) of matrix `layer`, or elements

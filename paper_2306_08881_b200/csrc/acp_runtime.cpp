@@ -351,10 +351,16 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
         continue;
       }
       const double bpe = mode == 0 ? 12.0 : (mode == 2 ? 16.0 : 8.0);
-      const bool fast = L.sm[mi].tr > 0;
-      const int64_t tr = fast ? L.sm[mi].tr : 1;
-      if (fast) stage_floats = std::max<int64_t>(stage_floats, tr * L.m);
-      units.push_back({i, -1, L.n, bpe * (double)L.m, tr});
+      const StreamMap& mp = L.sm[mi];
+      const bool fast = mp.tr > 0;
+      const int64_t tr = fast ? mp.tr : 1;
+      const int64_t pc = fast ? mp.pcols : L.m;
+      const int np = fast ? mp.np : 1;
+      if (fast) stage_floats = std::max<int64_t>(stage_floats, tr * pc);
+      for (int pn = 0; pn < np; ++pn) {
+        const int64_t cols = std::min<int64_t>(pc, L.m - (int64_t)pn * pc);
+        units.push_back({i, pn, L.n, bpe * (double)cols, tr});
+      }
       bytes += bpe * (double)L.n * (double)L.m;
       if (mode == 0) bytes += 4.0 * L.r * (double)(L.m + L.n);
       if (mode == 2) bytes += 4.0 * L.r * (double)(2 * L.m + L.n);
@@ -372,27 +378,45 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
     ln.stages = std::max(2, stages);
     ln.stage_floats = (int)stage_floats;
     int64_t part = 0;
-    std::vector<int64_t> first_slot(P.T, -1), nslots(P.T, 0);
+    int counters = 0;
+    int prev_layer = -1, prev_panel = -1;
+    size_t unit_first = 0;
+    int64_t unit_slots = 0;
+    auto close_unit = [&]() {
+      for (size_t k = unit_first; k < P.streamsegs.size(); ++k) P.streamsegs[k].pcount = (int)unit_slots;
+    };
     ln.ncta = split_units(units, min_share, nsm * cps, P.ctab, [&](const Unit& u, int64_t a, int64_t b) {
       StreamSeg s{};
       s.layer = u.layer;
       s.row0 = a;
       s.row1 = b;
+      s.panel = u.panel < 0 ? 0 : u.panel;
       const LayerDesc& L = P.L[u.layer];
       if (mode == 3 && L.mat) {
+        if (u.layer != prev_layer || u.panel != prev_panel) {
+          if (prev_layer >= 0) close_unit();
+          prev_layer = u.layer;
+          prev_panel = u.panel;
+          unit_first = P.streamsegs.size();
+          unit_slots = 0;
+          ++counters;
+        }
         const StreamMap& mp = L.sm[2];
+        const int64_t pc = mp.tr > 0 ? mp.pcols : L.m;
         s.nslot = mp.tr > 0 ? (mp.tr / mp.rs) : 1;  // row slots of the mapping
+        s.counter = counters - 1;
         s.part_off = part;
-        if (first_slot[u.layer] < 0) first_slot[u.layer] = part;
-        s.pidx = (int)nslots[u.layer];
-        nslots[u.layer] += s.nslot;
-        part += (int64_t)s.nslot * round4((int64_t)L.r * L.m);
+        s.pidx = (int)unit_slots;
+        unit_slots += s.nslot;
+        part += (int64_t)s.nslot * round4((int64_t)L.r * pc);
       }
       P.streamsegs.push_back(s);
     });
-    for (int64_t k = ln.seg_off; k < (int64_t)P.streamsegs.size(); ++k)
-      P.streamsegs[k].pcount = (int)nslots[P.streamsegs[k].layer];
-    if (mode == 3) P.colpart_elems = std::max(P.colpart_elems, part);
+    if (mode == 3 && prev_layer >= 0) close_unit();
+    if (mode == 3) {
+      P.colpart_elems = std::max(P.colpart_elems, part);
+      P.colcnt_n = std::max<int64_t>(P.colcnt_n, counters);
+    }
     ln.bytes = bytes;
     return ln;
   };

@@ -41,7 +41,8 @@ template <> struct Cfg<2> { static constexpr int NW = 8, CPS = 1, TT = 4096; };
 template <> struct Cfg<3> { static constexpr int NW = 8, CPS = 1, TT = 8192; };
 
 __host__ __device__ constexpr int nc_max(int mode, int RT) {
-  return mode == 2 ? (RT <= 4 ? 3 : 1) : (RT <= 4 ? 4 : (RT == 8 ? 2 : 0));
+  return mode == 0 ? (RT <= 4 ? 5 : (RT == 8 ? 2 : 0))
+                   : (mode == 2 ? (RT <= 4 ? 3 : (RT == 8 ? 1 : 0)) : (RT <= 4 ? 4 : (RT == 8 ? 2 : 0)));
 }
 
 __device__ __forceinline__ uint32_t s32(const void* p) {
@@ -148,17 +149,31 @@ __device__ void producer(const Tables& t, const StreamSeg* segs, int sb, int se,
     const LayerDesc& L = t.layers[s.layer];
     const float* grad = t.grads[s.layer];
     if (!is_fast<MODE>(L, grad)) continue;
+    const StreamMap mp = L.sm[ModeIdx<MODE>::v];
     const int64_t m = L.m;
-    const int tr = L.sm[ModeIdx<MODE>::v].tr;
-    const float* pm = grad + s.row0 * m;
-    const float* pe = t.E + L.e_off + s.row0 * m;
+    const int tr = mp.tr;
+    const int64_t c0 = (int64_t)s.panel * mp.pcols;
+    const int64_t cols = (m - c0) < mp.pcols ? (m - c0) : mp.pcols;
+    const float* pm = grad + s.row0 * m + c0;
+    const float* pe = t.E + L.e_off + s.row0 * m + c0;
     for (int64_t r0 = s.row0; r0 < s.row1; r0 += tr) {
       const int64_t nr = (s.row1 - r0) < tr ? (s.row1 - r0) : tr;
-      const uint32_t bytes = (uint32_t)(nr * m * 4);
       mbar_wait(&sh.empty[stage], phase ^ 1u);
-      mbar_arrive_tx(&sh.full[stage], 2 * bytes);
-      bulk_g2s(sh.sM + (size_t)stage * sh.stage_floats, pm, bytes, &sh.full[stage], pol);
-      bulk_g2s(sh.sE + (size_t)stage * sh.stage_floats, pe, bytes, &sh.full[stage], pol);
+      float* dM = sh.sM + (size_t)stage * sh.stage_floats;
+      float* dE = sh.sE + (size_t)stage * sh.stage_floats;
+      if (cols == m) {  // whole rows: one contiguous copy per tensor
+        const uint32_t bytes = (uint32_t)(nr * m * 4);
+        mbar_arrive_tx(&sh.full[stage], 2 * bytes);
+        bulk_g2s(dM, pm, bytes, &sh.full[stage], pol);
+        bulk_g2s(dE, pe, bytes, &sh.full[stage], pol);
+      } else {          // panel: one copy per row, smem row stride pcols
+        const uint32_t rb = (uint32_t)(cols * 4);
+        mbar_arrive_tx(&sh.full[stage], (uint32_t)(2 * nr) * rb);
+        for (int64_t i = 0; i < nr; ++i) {
+          bulk_g2s(dM + i * mp.pcols, pm + i * m, rb, &sh.full[stage], pol);
+          bulk_g2s(dE + i * mp.pcols, pe + i * m, rb, &sh.full[stage], pol);
+        }
+      }
       pm += nr * m;
       pe += nr * m;
       if (++stage == sh.stages) {
@@ -186,8 +201,10 @@ __device__ void seg_fast(const Tables& t, const LayerDesc& L, const StreamSeg& s
   const int NRS = (NW / gw) * (32 / lg);
   const int m = (int)L.m;
   const int n = (int)L.n;
-  const int m4 = m >> 2;
   const int r = L.r;
+  const int pc = mp.pcols;                         // smem row stride (floats)
+  const int c0 = s.panel * pc;                     // first column of the panel
+  const int m4 = ((m - c0) < pc ? (m - c0) : pc) >> 2;  // chunks in this panel
   const int cbase = sub * lg * NC + li;
   int coff[NC];
   bool cval[NC];
@@ -197,7 +214,8 @@ __device__ void seg_fast(const Tables& t, const LayerDesc& L, const StreamSeg& s
     cval[i] = c < m4;
     coff[i] = 4 * (cval[i] ? c : 0);
   }
-  float* __restrict__ E = t.E + L.e_off;
+  float* __restrict__ E = t.E + L.e_off + c0;      // panel origin (global)
+  grad += c0;
   const float* __restrict__ Pf = t.pbuf + L.p_off;  // k-major [r][n]
 
   // factor(s) in registers for the whole segment (k >= r and invalid chunks: 0)
@@ -205,8 +223,8 @@ __device__ void seg_fast(const Tables& t, const LayerDesc& L, const StreamSeg& s
   float4 qb[MODE == 2 ? NC : 1][MODE == 2 ? RT : 1];
   float4 acc3[MODE == 3 ? NC : 1][MODE == 3 ? RT : 1];
   if constexpr (MODE != 3) {
-    const float* Qf = t.qbuf + L.q_off;
-    const float* Ql = t.qloc + L.ql_off;
+    const float* Qf = t.qbuf + L.q_off + c0;
+    const float* Ql = t.qloc + L.ql_off + c0;
 #pragma unroll
     for (int i = 0; i < NC; ++i)
 #pragma unroll
@@ -232,7 +250,7 @@ __device__ void seg_fast(const Tables& t, const LayerDesc& L, const StreamSeg& s
       const int tri = rowslot + NRS * j;  // row within the tile
       const bool rval = tri < nr;
       const int64_t row = r0 + (rval ? tri : 0);
-      const int toff = (rval ? tri : 0) * m;
+      const int toff = (rval ? tri : 0) * pc;
       float4 x[NC];
 #pragma unroll
       for (int i = 0; i < NC; ++i) {
@@ -340,15 +358,15 @@ __device__ void seg_fast(const Tables& t, const LayerDesc& L, const StreamSeg& s
     pp.advance(sh.stages);
   }
   if constexpr (MODE == 3) {
-    // partial slot `rowslot` of this segment: k-major [r][m], 16-byte stride
-    const int64_t stride = ((int64_t)r * m + 3) & ~int64_t(3);
+    // partial slot `rowslot` of this segment: k-major [r][pc], 16-byte stride
+    const int64_t stride = ((int64_t)r * pc + 3) & ~int64_t(3);
     float* part = t.colpart + s.part_off + (int64_t)rowslot * stride;
 #pragma unroll
     for (int i = 0; i < NC; ++i) {
       if (cval[i]) {
 #pragma unroll
         for (int k = 0; k < RT; ++k)
-          if (k < r) *reinterpret_cast<float4*>(part + (int64_t)k * m + coff[i]) = acc3[i][k];
+          if (k < r) *reinterpret_cast<float4*>(part + (int64_t)k * pc + coff[i]) = acc3[i][k];
       }
     }
   }
@@ -389,12 +407,17 @@ __device__ void seg_generic(const Tables& t, const LayerDesc& L, const StreamSeg
   const float* __restrict__ Ql = t.qloc + L.ql_off;
   float* __restrict__ Ps = t.pbuf + L.p_off;
   float* __restrict__ E = t.E + L.e_off;
+  // column range of this segment's panel (modes 2, 3; generic layers have one)
+  const StreamMap mp = L.sm[ModeIdx<MODE>::v];
+  const int64_t pc = (MODE != 0 && mp.tr > 0) ? mp.pcols : m;
+  const int64_t c0 = (int64_t)s.panel * pc;
+  const int64_t c1 = (c0 + pc) < m ? (c0 + pc) : m;
   if constexpr (MODE == 3) {
     float* part = t.colpart + s.part_off;
-    const int64_t stride = ((int64_t)r * m + 3) & ~int64_t(3);
-    for (int64_t c0 = 0; c0 < m; c0 += NT) {
-      const int64_t c = c0 + threadIdx.x;
-      if (c < m) {
+    const int64_t stride = ((int64_t)r * pc + 3) & ~int64_t(3);
+    for (int64_t cb = c0; cb < c1; cb += NT) {
+      const int64_t c = cb + threadIdx.x;
+      if (c < c1) {
         float acc[RT];
 #pragma unroll
         for (int k = 0; k < RT; ++k) acc[k] = 0.f;
@@ -406,9 +429,9 @@ __device__ void seg_generic(const Tables& t, const LayerDesc& L, const StreamSeg
         }
 #pragma unroll
         for (int k = 0; k < RT; ++k)
-          if (k < r) part[k * m + c] = acc[k];
+          if (k < r) part[k * pc + (c - c0)] = acc[k];
         for (int gsl = 1; gsl < s.nslot; ++gsl)
-          for (int k = 0; k < r; ++k) part[(int64_t)gsl * stride + k * m + c] = 0.f;
+          for (int k = 0; k < r; ++k) part[(int64_t)gsl * stride + k * pc + (c - c0)] = 0.f;
       }
     }
     return;
@@ -443,7 +466,7 @@ __device__ void seg_generic(const Tables& t, const LayerDesc& L, const StreamSeg
       float p[RT];
 #pragma unroll
       for (int k = 0; k < RT; ++k) p[k] = (k < r) ? __ldg(Ps + k * n + row) : 0.f;
-      for (int64_t j = threadIdx.x; j < m; j += NT) {
+      for (int64_t j = c0 + threadIdx.x; j < c1; j += NT) {
         float x = gr[j] + er[j], o = 0.f;
 #pragma unroll
         for (int k = 0; k < RT; ++k) {
@@ -466,7 +489,7 @@ __device__ void col_finish(const Tables& t, const LayerDesc& L, const StreamSeg&
   __threadfence();
   cta_sync1<NT>();
   if (threadIdx.x == 0) {
-    const int old = atomicAdd(t.colcnt + s.layer, s.nslot);
+    const int old = atomicAdd(t.colcnt + s.counter, s.nslot);
     *flag = (old + s.nslot == s.pcount);
   }
   cta_sync1<NT>();
@@ -474,28 +497,23 @@ __device__ void col_finish(const Tables& t, const LayerDesc& L, const StreamSeg&
   __threadfence();
   const int64_t m = L.m;
   const int r = L.r;
-  const int64_t slot = ((int64_t)r * m + 3) & ~int64_t(3);
+  const StreamMap mp = L.sm[2];
+  const int64_t pc = mp.tr > 0 ? mp.pcols : m;   // generic layers: one full-width panel
+  const int64_t c0 = (int64_t)s.panel * pc;
+  const int64_t cols = (m - c0) < pc ? (m - c0) : pc;
+  const int64_t slot = ((int64_t)r * pc + 3) & ~int64_t(3);
   const float* first = t.colpart + s.part_off - (int64_t)s.pidx * slot;
-  float* Qs = t.qbuf + L.q_off;
-  float* Ql = t.qloc + L.ql_off;
-  const int64_t total = (int64_t)r * m;
-  if ((m & 3) == 0) {
-    for (int64_t i = 4 * threadIdx.x; i < total; i += 4 * NT) {
-      float4 acc = __ldcg(reinterpret_cast<const float4*>(first + i));
-      for (int p = 1; p < s.pcount; ++p)
-        acc = f4add(acc, __ldcg(reinterpret_cast<const float4*>(first + p * slot + i)));
-      *reinterpret_cast<float4*>(Qs + i) = acc;
-      *reinterpret_cast<float4*>(Ql + i) = acc;
-    }
-  } else {
-    for (int64_t i = threadIdx.x; i < total; i += NT) {
-      float acc = __ldcg(first + i);
-      for (int p = 1; p < s.pcount; ++p) acc += __ldcg(first + p * slot + i);
-      Qs[i] = acc;
-      Ql[i] = acc;
-    }
+  float* Qs = t.qbuf + L.q_off + c0;
+  float* Ql = t.qloc + L.ql_off + c0;
+  const int64_t total = (int64_t)r * cols;
+  for (int64_t i = threadIdx.x; i < total; i += NT) {
+    const int64_t k = i / cols, j = i - k * cols;
+    float acc = __ldcg(first + k * pc + j);
+    for (int p = 1; p < s.pcount; ++p) acc += __ldcg(first + p * slot + k * pc + j);
+    Qs[k * m + j] = acc;
+    Ql[k * m + j] = acc;
   }
-  if (threadIdx.x == 0) t.colcnt[s.layer] = 0;  // re-arm
+  if (threadIdx.x == 0) t.colcnt[s.counter] = 0;  // re-arm
 }
 
 template <int MODE, int RT>
@@ -559,6 +577,7 @@ __global__ void __launch_bounds__(Cfg<MODE>::NW * 32 + 32, Cfg<MODE>::CPS)
         ACP_CASE(2)
         ACP_CASE(3)
         ACP_CASE(4)
+        ACP_CASE(5)
 #undef ACP_CASE
         default: break;
       }
@@ -600,18 +619,27 @@ int stream_ctas_per_sm(int mode) {
 }
 
 bool stream_make_map(int mode, int64_t m, int rt, StreamMap* out) {
-  *out = StreamMap{0, 0, 0, 0, 0};
+  *out = StreamMap{};
   if (m % 4 != 0 || rt > 8) return false;
   const int NW = mode == 0 ? Cfg<0>::NW : (mode == 2 ? Cfg<2>::NW : Cfg<3>::NW);
   const int64_t TT = mode == 0 ? Cfg<0>::TT : (mode == 2 ? Cfg<2>::TT : Cfg<3>::TT);
   const int ncm = nc_max(mode, rt);
   if (ncm <= 0) return false;
   const int64_t m4 = m / 4;
-  if (m4 < 32) {  // sub-warp row groups
+  // panels (modes 2, 3): at most NW*32*ncm chunks each
+  int64_t np = 1, pc4 = m4;
+  if (mode != 0) {
+    np = (m4 + (int64_t)NW * 32 * ncm - 1) / ((int64_t)NW * 32 * ncm);
+    pc4 = (m4 + np - 1) / np;
+  }
+  const int64_t pcols = 4 * pc4;
+  out->np = (int16_t)np;
+  out->pcols = (int32_t)pcols;
+  if (pc4 < 32) {  // sub-warp row groups
     int lg = 1;
-    while (lg < m4) lg <<= 1;
+    while (lg < pc4) lg <<= 1;
     const int64_t nrs = (int64_t)NW * (32 / lg);
-    const int64_t rs = std::max<int64_t>(1, TT / (nrs * m));
+    const int64_t rs = std::max<int64_t>(1, TT / (nrs * pcols));
     out->lg = (int16_t)lg;
     out->gw = 1;
     out->nc = 1;
@@ -620,11 +648,11 @@ bool stream_make_map(int mode, int64_t m, int rt, StreamMap* out) {
     return true;
   }
   for (int gw = 1; gw <= NW; gw <<= 1) {
-    const int64_t nc = (m4 + 32LL * gw - 1) / (32LL * gw);
+    const int64_t nc = (pc4 + 32LL * gw - 1) / (32LL * gw);
     if (nc > ncm) continue;
     const int64_t nrs = NW / gw;
-    if (gw < NW && nrs * m > TT) continue;  // tile would exceed the target
-    const int64_t rs = std::max<int64_t>(1, TT / (nrs * m));
+    if (gw < NW && nrs * pcols > TT) continue;  // tile would exceed the target
+    const int64_t rs = std::max<int64_t>(1, TT / (nrs * pcols));
     out->lg = 32;
     out->gw = (int16_t)gw;
     out->nc = (int16_t)nc;
@@ -632,6 +660,7 @@ bool stream_make_map(int mode, int64_t m, int rt, StreamMap* out) {
     out->tr = (int32_t)(nrs * rs);
     return true;
   }
+  *out = StreamMap{};
   return false;
 }
 
