@@ -194,6 +194,8 @@ def _setup_dist(args):
 
 
 def _measure(model, r, world, rank, local, args, comm, profile=True):
+    """Time K steps (CUDA-graph replay, the library default), then K more
+    steps run eagerly with per-kernel CUDA events for the roofline."""
     import torch
     from paper_2306_08881_b200 import AcpContext
     shapes = _shapes(model)
@@ -206,15 +208,13 @@ def _measure(model, r, world, rank, local, args, comm, profile=True):
         grads.append((g / (m ** 0.5)).contiguous())
     ctx = AcpContext(shapes, r, world_size=world, nccl_comm=comm, seed=7,
                      bucket_bytes=args.bucket_bytes)
+    ctx.set_graphs(not args.no_graphs)
     stream = torch.cuda.current_stream()
     for t in range(args.warmup):
         ctx.step(grads, t % 2)
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
-    if profile:
-        ctx.profile(True)
-        ctx.profile_reset()
     l0 = ctx.launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
@@ -234,8 +234,16 @@ def _measure(model, r, world, rank, local, args, comm, profile=True):
         t = torch.tensor([ms], device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
-    prof = ctx.profile_read() if profile else None
-    ctx.profile(False)
+    prof = None
+    if profile:
+        # per-kernel CUDA events on the launching stream (eager launches)
+        ctx.profile(True)
+        ctx.profile_reset()
+        for t in range(args.steps):
+            ctx.step(grads, (args.warmup + args.steps + t) % 2)
+        torch.cuda.synchronize()
+        prof = ctx.profile_read()
+        ctx.profile(False)
     nb = (len(ctx.buckets(0)), len(ctx.buckets(1)))
     return {"ctx": ctx, "grads": grads, "shapes": shapes, "nel": nel, "ms": ms, "prof": prof,
             "launches": launches, "clocks": clk.summary(), "buckets": nb}
@@ -375,6 +383,7 @@ def main(argv=None):
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graphs", action="store_true")
     ap.add_argument("--oracle-every", type=int, default=3)
     args = ap.parse_args(argv)
     if args.warmup < 3:

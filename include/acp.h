@@ -164,6 +164,13 @@ acp_status acp_profile_reset(acp_ctx* ctx);
 acp_status acp_profile_read(acp_ctx* ctx, int32_t kernel_class, double* ms, int64_t* launches,
                             double* algorithmic_bytes);
 
+/* CUDA graphs (default on): the first acp_step of each parity is captured
+ * into a graph (kernels + NCCL calls) that later steps replay with a single
+ * launch; the gradient pointers are read from a device table refreshed
+ * before each launch, so new pointers do not need a new capture. Profiling
+ * (acp_profile_enable) always runs eagerly. */
+acp_status acp_set_graphs(acp_ctx* ctx, int32_t enable);
+
 /* Number of kernels this context has launched so far (its own kernels, not
  * NCCL's). */
 acp_status acp_launch_count(acp_ctx* ctx, int64_t* out);

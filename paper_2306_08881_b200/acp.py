@@ -115,14 +115,19 @@ class AcpContext:
 
     # -- helpers --------------------------------------------------------------
     def _grad_ptrs(self, grads):
+        """Pointer array for the C call. Tensors are validated only when the
+        pointer set changes (the per-step cost is one data_ptr() per tensor)."""
         import torch
         if len(grads) != len(self.shapes):
             raise ValueError(f"expected {len(self.shapes)} gradients, got {len(grads)}")
-        for i, (g, s) in enumerate(zip(grads, self.shapes)):
-            if not (isinstance(g, torch.Tensor) and g.is_cuda and g.dtype == torch.float32
-                    and g.is_contiguous() and g.numel() == int(np.prod(s))):
-                raise ValueError(f"gradient {i} must be a contiguous fp32 CUDA tensor of shape {s}")
-            self._ptrs[i] = g.data_ptr()
+        ptrs = [g.data_ptr() for g in grads]
+        if ptrs != getattr(self, "_last_ptrs", None):
+            for i, (g, s) in enumerate(zip(grads, self.shapes)):
+                if not (isinstance(g, torch.Tensor) and g.is_cuda and g.dtype == torch.float32
+                        and g.is_contiguous() and g.numel() == int(np.prod(s))):
+                    raise ValueError(f"gradient {i} must be a contiguous fp32 CUDA tensor of shape {s}")
+                self._ptrs[i] = ptrs[i]
+            self._last_ptrs = ptrs
         return C.cast(self._ptrs, C.POINTER(C.c_void_p))
 
     # -- hot path -------------------------------------------------------------
@@ -194,6 +199,9 @@ class AcpContext:
             L.check(self._lib.acp_profile_read(self._ctx, k, C.byref(ms), C.byref(n), C.byref(by)))
             out[name] = {"ms": ms.value, "launches": n.value, "bytes": by.value}
         return out
+
+    def set_graphs(self, enable: bool = True) -> None:
+        L.check(self._lib.acp_set_graphs(self._ctx, 1 if enable else 0))
 
     def launch_count(self) -> int:
         n = C.c_int64()

@@ -8,8 +8,7 @@ namespace acp {
 
 constexpr int kThreads = 256;          // every hot kernel runs 256-thread CTAs
 constexpr int kMaxV = 8;               // row kernel: float4 chunks per thread per row
-constexpr int kOrthRowsPerSeg = 1024;  // K2 work unit (factor rows)
-constexpr int kOrthChunk = 64;         // K2 smem staging (rows)
+constexpr int kOrthRowsPerSeg = 256;   // K2 work unit (factor rows), staged at once
 
 // Thread mapping of a matrix layer onto a TMA stream kernel CTA (NW warps):
 // a row is covered by `gw` warps (lg = 32) or by `lg` lanes of one warp
@@ -110,6 +109,7 @@ struct Tables {
   double* wmat;
   int32_t* orthcnt;
   uint32_t* degmask;
+  int64_t* step;         // device step counter (keys the method's random draws)
 };
 
 // launches (all on `stream`, 256 threads, grid = ncta)
@@ -124,6 +124,8 @@ cudaError_t launch_col(int rt, const Tables& t, const ColSeg* segs, const int32_
                        int ncta, int ef, cudaStream_t stream);
 // TMA-pipelined streaming kernels (k_stream.cu): mode 0 K1 P-step, mode 2 K3
 // Q-step, mode 3 K1 Q-step. rt <= 8, error feedback on.
+// Raise the dynamic shared-memory limit of a kernel once per device.
+cudaError_t allow_max_smem(const void* kern);
 cudaError_t launch_stream(int mode, int rt, const Tables& t, const StreamSeg* segs,
                           const int32_t* cta_begin, int ncta, float scale, int stages,
                           int stage_floats, cudaStream_t stream);
@@ -135,7 +137,9 @@ size_t stream_smem_bytes(int stages, int stage_floats);
 cudaError_t launch_orth(int rt, const Tables& t, int side, const OrthSeg* segs, int nseg,
                         uint64_t seed, int64_t step, cudaStream_t stream, int* launches);
 // Fill factor slots with counter-based N(0,1) (tag, step): side as above, or
-// side 2 = Q_0 into the Q-buffer. Layers = all matrices.
+// side 2 = Q_0 into the Q-buffer. Layers = all matrices. step < 0: use the
+// device step counter (*t.step). The orthogonaliser reads *t.step and its
+// last phase increments it, so a captured CUDA graph stays valid.
 cudaError_t launch_fill(const Tables& t, const LayerDesc* host_layers, int num_tensors, int side,
                         uint64_t seed, int tag, int64_t step, cudaStream_t stream, int* launches);
 // k-major slot <-> row-major rows x r (state access)

@@ -74,7 +74,7 @@ struct Plan {
   size_t off_E = 0, off_P = 0, off_Q = 0, off_QL = 0, off_colpart = 0, off_colcnt = 0,
          off_gram = 0, off_wmat = 0, off_orthcnt = 0, off_degmask = 0, off_layers = 0,
          off_grads = 0, off_rowsegs = 0, off_colsegs = 0, off_streamsegs = 0, off_orth[2] = {0, 0},
-         off_ctab = 0,
+         off_ctab = 0, off_step = 0,
          total = 0;
 };
 
@@ -494,6 +494,7 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
   P.off_orth[0] = take(sizeof(OrthSeg) * P.orthsegs[0].size());
   P.off_orth[1] = take(sizeof(OrthSeg) * P.orthsegs[1].size());
   P.off_ctab = take(4 * P.ctab.size());
+  P.off_step = take(8);
   P.total = o;
   return ACP_OK;
 }
@@ -534,6 +535,12 @@ struct acp_ctx {
   std::vector<ProfRec> prof;
   size_t prof_used = 0;
   ncclComm_t comm = nullptr;
+  // CUDA graphs: one captured step per parity (kernels read the gradient
+  // table and the step counter from device memory, so the graph is reusable)
+  bool use_graphs = true;
+  cudaStream_t cap_stream = nullptr;
+  cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+  int64_t graph_kernels[2] = {0, 0};
 };
 
 namespace {
@@ -622,15 +629,14 @@ acp_status run_orth(acp_ctx* c, int parity, cudaStream_t s) {
   const int side = parity == 0 ? 0 : 1;  // P-step orthogonalises Q, Q-step P
   int nl = 0;
   if (c->cfg.flags & ACP_NO_REUSE) {
-    cudaError_t e = launch_fill(c->tab, c->P.L.data(), c->P.T, side, c->cfg.seed, 3,
-                                c->step_count, s, &nl);
+    cudaError_t e = launch_fill(c->tab, c->P.L.data(), c->P.T, side, c->cfg.seed, 3, -1, s, &nl);
     if (e != cudaSuccess) return cuda_fail(c, e, "fill kernel launch");
   }
   const auto& segs = c->P.orthsegs[side];
   ProfRec* r = prof_begin(c, ACP_K_ORTH, c->P.orth_bytes[side], s);
   cudaError_t e = launch_orth(c->P.RT, c->tab, side,
                               reinterpret_cast<const OrthSeg*>(c->ws + c->P.off_orth[side]),
-                              (int)segs.size(), c->cfg.seed, c->step_count, s, &nl);
+                              (int)segs.size(), c->cfg.seed, -1, s, &nl);
   prof_end(r, s);
   c->launches += nl;
   if (e != cudaSuccess) return cuda_fail(c, e, "orthogonalisation kernel launch");
@@ -716,6 +722,7 @@ acp_status acp_create(const acp_config* cfg, acp_ctx** out) {
   t.wmat = reinterpret_cast<double*>(c->ws + P.off_wmat);
   t.orthcnt = reinterpret_cast<int32_t*>(c->ws + P.off_orthcnt);
   t.degmask = reinterpret_cast<uint32_t*>(c->ws + P.off_degmask);
+  t.step = reinterpret_cast<int64_t*>(c->ws + P.off_step);
 
   DeviceGuard dg(cfg->device);
   cudaStream_t s = nullptr;
@@ -775,6 +782,69 @@ acp_status acp_create(const acp_config* cfg, acp_ctx** out) {
   return ACP_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+// Enqueue one whole step (orthogonalise, per-bucket projection + all-reduce,
+// decode) on stream s; used eagerly and for graph capture.
+acp_status enqueue_step(acp_ctx* c, int32_t parity, cudaStream_t s) {
+  acp_status st;
+  if ((st = run_orth(c, parity, s)) != ACP_OK) return st;
+  const Plan& P = c->P;
+  if (c->cfg.world_size == 1) {
+    if ((st = run_k1(c, parity, P.k1_all[parity], s)) != ACP_OK) return st;
+    if ((st = run_k3(c, parity, P.k3_all[parity], s)) != ACP_OK) return st;
+    return ACP_OK;
+  }
+  float* buf = parity == 0 ? c->tab.pbuf : c->tab.qbuf;
+  const size_t nb = P.buckets[parity].size();
+  for (size_t b = 0; b < nb; ++b) {
+    if ((st = run_k1(c, parity, P.k1_b[parity][b], s)) != ACP_OK) return st;
+    CK(c, cudaEventRecord(c->ev_k1[b], s), "event record");
+    CK(c, cudaStreamWaitEvent(c->comm_stream, c->ev_k1[b], 0), "stream wait");
+    ProfRec* r = prof_begin(c, ACP_K_ALLREDUCE, 4.0 * P.bcnt[parity][b], c->comm_stream);
+    ncclResult_t nr = ncclAllReduce(buf + P.boff[parity][b], buf + P.boff[parity][b],
+                                    (size_t)P.bcnt[parity][b], ncclFloat, ncclSum, c->comm,
+                                    c->comm_stream);
+    prof_end(r, c->comm_stream);
+    if (nr != ncclSuccess) {
+      c->poisoned = true;
+      return fail(ACP_E_NCCL, std::string("ncclAllReduce: ") + ncclGetErrorString(nr));
+    }
+    CK(c, cudaEventRecord(c->ev_ar[b], c->comm_stream), "event record");
+  }
+  for (size_t b = 0; b < nb; ++b) {
+    CK(c, cudaStreamWaitEvent(s, c->ev_ar[b], 0), "stream wait");
+    if ((st = run_k3(c, parity, P.k3_b[parity][b], s)) != ACP_OK) return st;
+  }
+  return ACP_OK;
+}
+
+acp_status capture_step(acp_ctx* c, int32_t parity) {
+  if (!c->cap_stream) CK(c, cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking), "capture stream");
+  const int64_t l0 = c->launches;
+  CK(c, cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal), "begin capture");
+  acp_status st = enqueue_step(c, parity, c->cap_stream);
+  cudaGraph_t g = nullptr;
+  cudaError_t e = cudaStreamEndCapture(c->cap_stream, &g);
+  if (st != ACP_OK) {
+    if (g) cudaGraphDestroy(g);
+    return st;
+  }
+  if (e != cudaSuccess) return cuda_fail(c, e, "end capture");
+  e = cudaGraphInstantiate(&c->gexec[parity], g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) return cuda_fail(c, e, "graph instantiate");
+  c->graph_kernels[parity] = c->launches - l0;
+  c->launches = l0;
+  return ACP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
 acp_status acp_step(acp_ctx* c, int32_t parity, float* const* grads, void* stream) {
   acp_status st = check_ctx(c);
   if (st != ACP_OK) return st;
@@ -784,35 +854,20 @@ acp_status acp_step(acp_ctx* c, int32_t parity, float* const* grads, void* strea
   DeviceGuard dg(c->cfg.device);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if ((st = set_grads(c, grads, s)) != ACP_OK) return st;
-  if ((st = run_orth(c, parity, s)) != ACP_OK) return st;
-  const Plan& P = c->P;
-  if (c->cfg.world_size == 1) {
-    if ((st = run_k1(c, parity, P.k1_all[parity], s)) != ACP_OK) return st;
-    if ((st = run_k3(c, parity, P.k3_all[parity], s)) != ACP_OK) return st;
-  } else {
-    float* buf = parity == 0 ? c->tab.pbuf : c->tab.qbuf;
-    const size_t nb = P.buckets[parity].size();
-    for (size_t b = 0; b < nb; ++b) {
-      if ((st = run_k1(c, parity, P.k1_b[parity][b], s)) != ACP_OK) return st;
-      CK(c, cudaEventRecord(c->ev_k1[b], s), "event record");
-      CK(c, cudaStreamWaitEvent(c->comm_stream, c->ev_k1[b], 0), "stream wait");
-      ProfRec* r = prof_begin(c, ACP_K_ALLREDUCE, 4.0 * P.bcnt[parity][b], c->comm_stream);
-      ncclResult_t nr = ncclAllReduce(buf + P.boff[parity][b], buf + P.boff[parity][b],
-                                      (size_t)P.bcnt[parity][b], ncclFloat, ncclSum, c->comm,
-                                      c->comm_stream);
-      prof_end(r, c->comm_stream);
-      if (nr != ncclSuccess) {
-        c->poisoned = true;
-        return fail(ACP_E_NCCL, std::string("ncclAllReduce: ") + ncclGetErrorString(nr));
-      }
-      CK(c, cudaEventRecord(c->ev_ar[b], c->comm_stream), "event record");
-    }
-    for (size_t b = 0; b < nb; ++b) {
-      CK(c, cudaStreamWaitEvent(s, c->ev_ar[b], 0), "stream wait");
-      if ((st = run_k3(c, parity, P.k3_b[parity][b], s)) != ACP_OK) return st;
-    }
+  if (c->use_graphs && !c->profile) {
+    if (!c->gexec[parity] && (st = capture_step(c, parity)) != ACP_OK) return st;
+    CK(c, cudaGraphLaunch(c->gexec[parity], s), "graph launch");
+    c->launches += c->graph_kernels[parity];
+  } else if ((st = enqueue_step(c, parity, s)) != ACP_OK) {
+    return st;
   }
   ++c->step_count;
+  return ACP_OK;
+}
+
+acp_status acp_set_graphs(acp_ctx* c, int32_t enable) {
+  if (!c) return fail(ACP_E_INVAL, "ctx is NULL");
+  c->use_graphs = enable != 0;
   return ACP_OK;
 }
 
@@ -943,6 +998,9 @@ acp_status acp_launch_count(acp_ctx* c, int64_t* out) {
 acp_status acp_destroy(acp_ctx* c) {
   if (!c) return ACP_OK;
   DeviceGuard dg(c->cfg.device);
+  for (auto& ge : c->gexec)
+    if (ge) cudaGraphExecDestroy(ge);
+  if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   if (c->comm_stream) {
     cudaStreamSynchronize(c->comm_stream);
     cudaStreamDestroy(c->comm_stream);

@@ -2,7 +2,7 @@
 // "Orthogonalize" = reduced-QR Q factor), batched over every layer.
 //
 // Algorithm: CholeskyQR2 with float64 Gram / Cholesky:
-//   phase 0: G1 = A^T A            (partial Gram per 1024-row segment, fp64)
+//   phase 0: G1 = A^T A            (partial Gram per 256-row segment, fp64)
 //            last segment of the layer: G1 = R1^T R1 (Cholesky), W1 = R1^-1
 //   phase 1: A1 = A W1  (columns flagged degenerate replaced by the seeded
 //            Gaussian column), G2 = A1^T A1, last segment: W2 = R2^-1
@@ -10,7 +10,7 @@
 // Q equals the reduced-QR factor with R_kk > 0 that the oracle's MGS2 computes
 // (same column space and orientation; DESIGN.md derives the degenerate case).
 // Unlike a per-layer Gram-Schmidt, every phase is a grid-wide data-parallel
-// sweep, so a 30522 x 32 factor is spread over 30 CTAs instead of serialising
+// sweep, so a 30522 x 32 factor is spread over 120 CTAs instead of serialising
 // 2r dependent reductions on one SM. The Gram partials are summed in a fixed
 // order (deterministic: every rank computes bit-identical factors).
 #include "k_common.cuh"
@@ -18,20 +18,27 @@
 namespace acp {
 namespace {
 
-constexpr int kCH = 32;              // factor rows staged per round
-constexpr double kDegTol2 = 1e-12;   // (1e-6)^2, reading C6
+constexpr int kSeg = kOrthRowsPerSeg;   // rows staged per CTA (one shot)
+constexpr int kLd = kSeg + 1;           // padded smem row (bank spread)
+constexpr double kDegTol2 = 1e-12;      // (1e-6)^2, reading C6
+
+template <int RT>
+constexpr size_t orth_smem() {
+  return (size_t)2 * RT * kLd * 4 + (size_t)3 * RT * RT * 8 + kThreads * 8 + 16;
+}
 
 template <int RT>
 __global__ void __launch_bounds__(kThreads) orth_kernel(Tables t, int side,
                                                         const OrthSeg* __restrict__ segs,
-                                                        int phase, uint64_t seed, int64_t step) {
-  __shared__ double A[RT][kCH + 1];
-  __shared__ double B[RT][kCH + 1];
-  __shared__ double Wm[RT * RT];
-  __shared__ double Gs[RT * RT];
-  __shared__ double Rm[RT * RT];
-  __shared__ double gred[kThreads];
-  __shared__ int flag;
+                                                        int phase, uint64_t seed) {
+  extern __shared__ __align__(16) unsigned char orth_smem_raw[];
+  float* A = reinterpret_cast<float*>(orth_smem_raw);  // [RT][kLd] input rows (fp32)
+  float* B = A + RT * kLd;                               // [RT][kLd] phase-1 output rows
+  double* Wm = reinterpret_cast<double*>(B + RT * kLd);  // [RT*RT]
+  double* Gs = Wm + RT * RT;
+  double* Rm = Gs + RT * RT;
+  double* gred = Rm + RT * RT;                            // [kThreads]
+  int* flag = reinterpret_cast<int*>(gred + kThreads);
 
   const OrthSeg s = segs[blockIdx.x];
   const LayerDesc L = t.layers[s.layer];
@@ -41,99 +48,93 @@ __global__ void __launch_bounds__(kThreads) orth_kernel(Tables t, int side,
   double* W1 = t.wmat + L.w_off;
   double* W2 = W1 + r * r;
   const int tid = threadIdx.x;
+  const int nr = (int)(s.row1 - s.row0);
+  const int64_t step = *t.step;
+  if (phase == 2 && blockIdx.x == 0 && tid == 0) {
+    // every CTA of phases 0-1 has read the step (stream order): advance it
+    *t.step = step + 1;
+  }
 
+  // stage the segment's rows (coalesced along rows, k-major source)
+  for (int idx = tid; idx < r * kSeg; idx += kThreads) {
+    const int k = idx / kSeg, i = idx - k * kSeg;
+    A[k * kLd + i] = i < nr ? F[(int64_t)k * len + s.row0 + i] : 0.f;
+  }
   uint32_t deg = 0;
   if (phase > 0) {
     const double* Wsrc = phase == 1 ? W1 : W2;
     for (int i = tid; i < r * r; i += kThreads) Wm[i] = Wsrc[i];
     if (phase == 1) deg = t.degmask[L.deg_idx];
   }
+  __syncthreads();
+  const float* G = A;  // rows the Gram is taken of
+  if (phase > 0) {
+    // apply W (upper triangular): out_l = sum_{k<=l} a_k W_kl; a column
+    // flagged degenerate becomes the seeded Gaussian column (reading C6)
+    for (int idx = tid; idx < r * kSeg; idx += kThreads) {
+      const int l = idx / kSeg, i = idx - l * kSeg;
+      float vf = 0.f;
+      if (i < nr) {
+        double v = 0.0;
+        if ((deg >> l) & 1u) {
+          v = (double)gaussian_at(column_key(seed, kTagDegenerate, (uint64_t)s.layer,
+                                             (uint64_t)step, (uint64_t)l),
+                                  (uint64_t)(s.row0 + i));
+        } else {
+          for (int k = 0; k <= l; ++k) v = fma((double)A[k * kLd + i], Wm[k * r + l], v);
+        }
+        vf = (float)v;
+        F[(int64_t)l * len + s.row0 + i] = vf;
+      }
+      B[l * kLd + i] = vf;
+    }
+    if (phase == 2) return;
+    __syncthreads();
+    G = B;
+  }
 
-  // Gram pair assignment: pair pi <-> (k, l), l <= k; S row splits per pair
+  // partial Gram of this segment (fp64): pair pi <-> (k, l), l <= k, with
+  // S row splits per pair
   const int NP = r * (r + 1) / 2;
   const int S = NP <= kThreads ? kThreads / NP : 1;
-  int pk[3], pl[3], npairs = 0;
   const int sp = NP <= kThreads ? tid % S : 0;
-  for (int j = 0; j < 3; ++j) {
-    const int pi = NP <= kThreads ? (j == 0 ? tid / S : NP) : tid + j * kThreads;
-    if (pi < NP) {
-      int k = 0;
-      while ((k + 1) * (k + 2) / 2 <= pi) ++k;
-      pk[npairs] = k;
-      pl[npairs] = pi - k * (k + 1) / 2;
-      ++npairs;
-    }
-  }
-  double acc[3] = {0.0, 0.0, 0.0};
-
-  for (int64_t ch0 = s.row0; ch0 < s.row1; ch0 += kCH) {
-    const int nr = (int)((s.row1 - ch0) < kCH ? (s.row1 - ch0) : kCH);
-    __syncthreads();
-    for (int idx = tid; idx < r * kCH; idx += kThreads) {
-      const int k = idx / kCH, i = idx - k * kCH;
-      A[k][i] = i < nr ? (double)F[(int64_t)k * len + ch0 + i] : 0.0;
-    }
-    __syncthreads();
-    if (phase > 0) {
-      for (int idx = tid; idx < r * kCH; idx += kThreads) {
-        const int l = idx / kCH, i = idx - l * kCH;
-        double v = 0.0;
-        if (i < nr) {
-          if ((deg >> l) & 1u) {
-            v = (double)gaussian_at(column_key(seed, kTagDegenerate, (uint64_t)s.layer,
-                                               (uint64_t)step, (uint64_t)l),
-                                    (uint64_t)(ch0 + i));
-          } else {
-            for (int k = 0; k <= l; ++k) v = fma(A[k][i], Wm[k * r + l], v);
-          }
-          const float vf = (float)v;
-          F[(int64_t)l * len + ch0 + i] = vf;
-          v = (double)vf;
-        }
-        B[l][i] = v;
-      }
-      __syncthreads();
-    }
-    if (phase < 2) {
-      for (int j = 0; j < npairs; ++j) {
-        const int k = pk[j], l = pl[j];
-        double a = acc[j];
-        if (phase == 0) {
-          for (int i = sp; i < nr; i += S) a = fma(A[k][i], A[l][i], a);
-        } else {
-          for (int i = sp; i < nr; i += S) a = fma(B[k][i], B[l][i], a);
-        }
-        acc[j] = a;
-      }
-    }
-  }
-  if (phase == 2) return;
-
-  // partial Gram of this segment (full symmetric r x r)
   double* part = t.gram + s.gram_off;
   if (NP <= kThreads) {
-    gred[tid] = acc[0];
+    const int pi = tid / S;
+    double a = 0.0;
+    int k = 0, l = 0;
+    if (pi < NP) {
+      while ((k + 1) * (k + 2) / 2 <= pi) ++k;
+      l = pi - k * (k + 1) / 2;
+      for (int i = sp; i < nr; i += S) a = fma((double)G[k * kLd + i], (double)G[l * kLd + i], a);
+    }
+    gred[tid] = a;
     __syncthreads();
-    if (sp == 0 && npairs > 0) {
+    if (sp == 0 && pi < NP) {
       double g = 0.0;
       for (int j = 0; j < S; ++j) g += gred[tid + j];
-      part[pk[0] * r + pl[0]] = g;
-      part[pl[0] * r + pk[0]] = g;
+      part[k * r + l] = g;
+      part[l * r + k] = g;
     }
   } else {
-    for (int j = 0; j < npairs; ++j) {
-      part[pk[j] * r + pl[j]] = acc[j];
-      part[pl[j] * r + pk[j]] = acc[j];
+    for (int pi = tid; pi < NP; pi += kThreads) {
+      int k = 0;
+      while ((k + 1) * (k + 2) / 2 <= pi) ++k;
+      const int l = pi - k * (k + 1) / 2;
+      double a = 0.0;
+      for (int i = 0; i < nr; ++i) a = fma((double)G[k * kLd + i], (double)G[l * kLd + i], a);
+      part[k * r + l] = a;
+      part[l * r + k] = a;
     }
   }
   __threadfence();
   __syncthreads();
   if (tid == 0) {
     const int old = atomicAdd(t.orthcnt + L.deg_idx, 1);
-    flag = (old == s.nseg - 1);
+    *flag = (old == s.nseg - 1);
   }
   __syncthreads();
-  if (!flag) return;
+  if (!*flag) return;
   __threadfence();
 
   // last segment of the layer: sum the partials in segment order
@@ -197,6 +198,7 @@ __global__ void __launch_bounds__(kThreads) orth_kernel(Tables t, int side,
 }
 
 __global__ void fill_kernel(Tables t, int side, uint64_t seed, int tag, int64_t step) {
+  if (step < 0) step = *t.step;
   const int layer = blockIdx.y;
   const LayerDesc L = t.layers[layer];
   if (!L.mat) return;
@@ -227,16 +229,25 @@ __global__ void transpose_kernel(const float* __restrict__ src, float* __restric
 cudaError_t launch_orth(int rt, const Tables& t, int side, const OrthSeg* segs, int nseg,
                         uint64_t seed, int64_t step, cudaStream_t s, int* launches) {
   if (nseg <= 0) return cudaSuccess;
+  (void)step;
+  auto go = [&](auto kern, size_t smem, int phase) -> cudaError_t {
+    cudaError_t e = allow_max_smem(reinterpret_cast<const void*>(kern));
+    if (e != cudaSuccess) return e;
+    kern<<<nseg, kThreads, smem, s>>>(t, side, segs, phase, seed);
+    return cudaSuccess;
+  };
   for (int phase = 0; phase < 3; ++phase) {
+    cudaError_t e0;
     switch (rt) {
-      case 1: orth_kernel<1><<<nseg, kThreads, 0, s>>>(t, side, segs, phase, seed, step); break;
-      case 2: orth_kernel<2><<<nseg, kThreads, 0, s>>>(t, side, segs, phase, seed, step); break;
-      case 4: orth_kernel<4><<<nseg, kThreads, 0, s>>>(t, side, segs, phase, seed, step); break;
-      case 8: orth_kernel<8><<<nseg, kThreads, 0, s>>>(t, side, segs, phase, seed, step); break;
-      case 16: orth_kernel<16><<<nseg, kThreads, 0, s>>>(t, side, segs, phase, seed, step); break;
-      case 32: orth_kernel<32><<<nseg, kThreads, 0, s>>>(t, side, segs, phase, seed, step); break;
+      case 1: e0 = go(orth_kernel<1>, orth_smem<1>(), phase); break;
+      case 2: e0 = go(orth_kernel<2>, orth_smem<2>(), phase); break;
+      case 4: e0 = go(orth_kernel<4>, orth_smem<4>(), phase); break;
+      case 8: e0 = go(orth_kernel<8>, orth_smem<8>(), phase); break;
+      case 16: e0 = go(orth_kernel<16>, orth_smem<16>(), phase); break;
+      case 32: e0 = go(orth_kernel<32>, orth_smem<32>(), phase); break;
       default: return cudaErrorInvalidValue;
     }
+    if (e0 != cudaSuccess) return e0;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     if (launches) ++*launches;

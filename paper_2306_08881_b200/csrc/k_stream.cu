@@ -22,6 +22,9 @@
 // register budget, gradient not 16-byte aligned) run a generic path in the
 // same launch; vectors (1-D params) are packed/unpacked here too.
 #include <algorithm>
+#include <mutex>
+#include <utility>
+#include <vector>
 
 #include "k_common.cuh"
 
@@ -591,8 +594,7 @@ cudaError_t launch_mode(int rt, const Tables& t, const StreamSeg* segs, const in
                         float scale, int stages, int stage_floats, cudaStream_t st) {
   const size_t smem = stream_smem_bytes(stages, stage_floats);
   auto go = [&](auto kern) -> cudaError_t {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+    cudaError_t e = allow_max_smem(reinterpret_cast<const void*>(kern));
     if (e != cudaSuccess) return e;
     kern<<<ncta, Cfg<MODE>::NW * 32 + 32, smem, st>>>(t, segs, cb, scale, stages, stage_floats);
     return cudaGetLastError();
@@ -607,6 +609,20 @@ cudaError_t launch_mode(int rt, const Tables& t, const StreamSeg* segs, const in
 }
 
 }  // namespace
+
+cudaError_t allow_max_smem(const void* kern) {
+  // one attribute call per (kernel, device); the table is tiny and process-wide
+  static std::mutex mu;
+  static std::vector<std::pair<const void*, int>> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto& d : done)
+    if (d.first == kern && d.second == dev) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  if (e == cudaSuccess) done.emplace_back(kern, dev);
+  return e;
+}
 
 size_t stream_smem_bytes(int stages, int stage_floats) {
   return (size_t)2 * stages * stage_floats * 4 + 2 * stages * 8 + (2 * 16 * 8 + 16 * 32) * 4 + 16;

@@ -193,3 +193,30 @@ def test_unaligned_gradients_take_generic_path():
         for a, b in zip(views, ref):
             assert rel_frobenius(a.cpu().numpy(), b) < TOL
     ctx.close()
+
+
+def test_graph_replay_matches_eager():
+    """acp_step replays a captured CUDA graph after the first step of each
+    parity; results must be bit-identical to eager launches (the step counter
+    and the gradient table live in device memory)."""
+    import torch
+    from paper_2306_08881_b200 import AcpContext
+    shapes = [(300, 1024), (1024,), (40, 4608), (64, 147), (8, 8)]
+    q0 = make_q0(shapes, 4, SEED)
+    outs = []
+    for graphs in (True, False):
+        ctx = AcpContext(shapes, 4, seed=SEED, q0=q0)
+        ctx.set_graphs(graphs)
+        res = []
+        for t in range(5):
+            g = [torch.from_numpy(np.random.default_rng([t, i]).standard_normal(s).astype(np.float32)).cuda()
+                 for i, s in enumerate(shapes)]
+            if t == 3:  # new gradient buffers: the device pointer table is refreshed
+                g = [x.clone() for x in g]
+            ctx.step(g, t % 2)
+            res.append([x.cpu().numpy() for x in g])
+        outs.append(res)
+        ctx.close()
+    for a, b in zip(*outs):
+        for x, y in zip(a, b):
+            assert np.array_equal(x, y)
