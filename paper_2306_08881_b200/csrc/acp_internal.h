@@ -96,6 +96,20 @@ struct OrthSeg {
   int32_t gram_first;  // segment index of the layer's first partial (gram_off of seg 0)
 };
 
+// K1 Q-step second stage: one (layer, panel) output unit. Items
+// [item_begin, item_end) of the flattened (k, float4 column) space.
+struct ColReduceTask {
+  int64_t part_first;   // float offset of the unit's first partial slot
+  int64_t stride;       // slot stride (floats)
+  int64_t pc;           // slot row length (panel width, floats)
+  int64_t cols;         // columns of this panel
+  int64_t m;            // layer width (Q slot row length)
+  int64_t q_dst, ql_dst;  // float offsets of column c0 of k-row 0 in the Q-buffer / local-Q copy
+  int32_t pcount;       // partial slots of the unit
+  int32_t item_begin, item_end;
+  int32_t pad_;
+};
+
 struct Tables {
   const LayerDesc* layers;
   float* const* grads;   // device table of gradient pointers
@@ -124,6 +138,8 @@ cudaError_t launch_col(int rt, const Tables& t, const ColSeg* segs, const int32_
                        int ncta, int ef, cudaStream_t stream);
 // TMA-pipelined streaming kernels (k_stream.cu): mode 0 K1 P-step, mode 2 K3
 // Q-step, mode 3 K1 Q-step. rt <= 8, error feedback on.
+cudaError_t launch_col_reduce(const Tables& t, const ColReduceTask* tasks, int ntasks, int nitems,
+                              cudaStream_t stream);
 // Raise the dynamic shared-memory limit of a kernel once per device.
 cudaError_t allow_max_smem(const void* kern);
 cudaError_t launch_stream(int mode, int rt, const Tables& t, const StreamSeg* segs,

@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -41,6 +42,8 @@ struct Launch {
   int64_t cb_off = 0;    // first entry of cta_begin
   int ncta = 0;
   int stages = 0, stage_floats = 0;
+  int64_t red_off = 0;   // K1 Q-step: first ColReduceTask of this launch
+  int nred = 0, nitems = 0;
   double bytes = 0;      // algorithmic bytes moved by this launch
 };
 
@@ -64,17 +67,23 @@ struct Plan {
   std::vector<RowSeg> rowsegs;
   std::vector<ColSeg> colsegs;
   std::vector<StreamSeg> streamsegs;
+  std::vector<ColReduceTask> redtasks;
   std::vector<OrthSeg> orthsegs[2];
   std::vector<int32_t> ctab;
   Launch k1_all[2], k3_all[2];
-  std::vector<Launch> k1_b[2], k3_b[2];
+  // world_size > 1: compute groups = runs of consecutive buckets whose
+  // projection / decode run as one launch; each bucket is still its own
+  // all-reduce (the paper's fusion rule), issued as an NCCL group per compute
+  // group as soon as the group's projection has finished.
+  std::vector<Launch> k1_g[2], k3_g[2];
+  std::vector<std::pair<int, int>> groups[2];  // [first bucket, last bucket]
   double orth_bytes[2] = {0, 0};
   int64_t colpart_elems = 0, colcnt_n = 1, gram_elems = 1;
   // workspace byte offsets
   size_t off_E = 0, off_P = 0, off_Q = 0, off_QL = 0, off_colpart = 0, off_colcnt = 0,
          off_gram = 0, off_wmat = 0, off_orthcnt = 0, off_degmask = 0, off_layers = 0,
          off_grads = 0, off_rowsegs = 0, off_colsegs = 0, off_streamsegs = 0, off_orth[2] = {0, 0},
-         off_ctab = 0, off_step = 0,
+         off_ctab = 0, off_step = 0, off_red = 0,
          total = 0;
 };
 
@@ -378,13 +387,8 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
     ln.stages = std::max(2, stages);
     ln.stage_floats = (int)stage_floats;
     int64_t part = 0;
-    int counters = 0;
     int prev_layer = -1, prev_panel = -1;
-    size_t unit_first = 0;
-    int64_t unit_slots = 0;
-    auto close_unit = [&]() {
-      for (size_t k = unit_first; k < P.streamsegs.size(); ++k) P.streamsegs[k].pcount = (int)unit_slots;
-    };
+    ln.red_off = (int64_t)P.redtasks.size();
     ln.ncta = split_units(units, min_share, nsm * cps, P.ctab, [&](const Unit& u, int64_t a, int64_t b) {
       StreamSeg s{};
       s.layer = u.layer;
@@ -393,30 +397,37 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
       s.panel = u.panel < 0 ? 0 : u.panel;
       const LayerDesc& L = P.L[u.layer];
       if (mode == 3 && L.mat) {
-        if (u.layer != prev_layer || u.panel != prev_panel) {
-          if (prev_layer >= 0) close_unit();
-          prev_layer = u.layer;
-          prev_panel = u.panel;
-          unit_first = P.streamsegs.size();
-          unit_slots = 0;
-          ++counters;
-        }
         const StreamMap& mp = L.sm[2];
         const int64_t pc = mp.tr > 0 ? mp.pcols : L.m;
-        s.nslot = mp.tr > 0 ? (mp.tr / mp.rs) : 1;  // row slots of the mapping
-        s.counter = counters - 1;
+        const int64_t stride = round4((int64_t)L.r * pc);
+        if (u.layer != prev_layer || u.panel != prev_panel) {
+          // new (layer, panel) output unit: its partial slots are contiguous
+          prev_layer = u.layer;
+          prev_panel = u.panel;
+          ColReduceTask tk{};
+          const int64_t c0 = (int64_t)s.panel * pc;
+          tk.part_first = part;
+          tk.stride = stride;
+          tk.pc = pc;
+          tk.cols = std::min<int64_t>(pc, L.m - c0);
+          tk.m = L.m;
+          tk.q_dst = L.q_off + c0;
+          tk.ql_dst = L.ql_off + c0;
+          tk.pcount = 0;
+          tk.item_begin = ln.nitems;
+          ln.nitems += (int)(L.r * ((tk.cols + 3) / 4));
+          tk.item_end = ln.nitems;
+          P.redtasks.push_back(tk);
+          ++ln.nred;
+        }
+        s.nslot = 1;
         s.part_off = part;
-        s.pidx = (int)unit_slots;
-        unit_slots += s.nslot;
-        part += (int64_t)s.nslot * round4((int64_t)L.r * pc);
+        s.pidx = P.redtasks.back().pcount++;
+        part += stride;
       }
       P.streamsegs.push_back(s);
     });
-    if (mode == 3 && prev_layer >= 0) close_unit();
-    if (mode == 3) {
-      P.colpart_elems = std::max(P.colpart_elems, part);
-      P.colcnt_n = std::max<int64_t>(P.colcnt_n, counters);
-    }
+    if (mode == 3) P.colpart_elems = std::max(P.colpart_elems, part);
     ln.bytes = bytes;
     return ln;
   };
@@ -436,10 +447,33 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
     P.k3_all[p] = k3_launch(p, all);
   }
   if (cfg->world_size > 1) {
+    int ngroups = 8;
+    if (const char* env = std::getenv("ACP_COMPUTE_GROUPS")) ngroups = std::max(1, std::atoi(env));
     for (int p = 0; p < 2; ++p) {
-      for (const auto& b : P.buckets[p]) {
-        P.k1_b[p].push_back(k1_launch(p, b));
-        P.k3_b[p].push_back(k3_launch(p, b));
+      // balance groups by gradient elements, cutting only at bucket boundaries
+      const int nb = (int)P.buckets[p].size();
+      std::vector<double> w(nb, 0.0);
+      double tot = 0;
+      for (int b = 0; b < nb; ++b) {
+        for (int i : P.buckets[p][b]) w[b] += P.L[i].mat ? (double)P.L[i].n * P.L[i].m : (double)P.L[i].n;
+        tot += w[b];
+      }
+      const int ng = std::min(ngroups, nb);
+      double acc = 0;
+      int first = 0, made = 0;
+      for (int b = 0; b < nb; ++b) {
+        acc += w[b];
+        const bool last = b == nb - 1;
+        if (last || (acc >= tot * (made + 1) / ng && made < ng - 1)) {
+          P.groups[p].push_back({first, b});
+          std::vector<int> ts;
+          for (int bb = first; bb <= b; ++bb)
+            ts.insert(ts.end(), P.buckets[p][bb].begin(), P.buckets[p][bb].end());
+          P.k1_g[p].push_back(k1_launch(p, ts));
+          P.k3_g[p].push_back(k3_launch(p, ts));
+          first = b + 1;
+          ++made;
+        }
       }
     }
   }
@@ -495,6 +529,7 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
   P.off_orth[1] = take(sizeof(OrthSeg) * P.orthsegs[1].size());
   P.off_ctab = take(4 * P.ctab.size());
   P.off_step = take(8);
+  P.off_red = take(sizeof(ColReduceTask) * P.redtasks.size());
   P.total = o;
   return ACP_OK;
 }
@@ -596,9 +631,16 @@ acp_status run_k1(acp_ctx* c, int parity, const Launch& ln, cudaStream_t s) {
   const int ef = c->P.ef ? 1 : 0;
   ProfRec* r = prof_begin(c, parity == 0 ? ACP_K_PROJ_P : ACP_K_PROJ_Q, ln.bytes, s);
   cudaError_t e;
-  if (ln.kind == 2)
+  if (ln.kind == 2) {
     e = launch_stream(ln.mode, c->P.RT, c->tab, dev_streamsegs(c, ln), dev_ctab(c, ln), ln.ncta,
                       1.0f, ln.stages, ln.stage_floats, s);
+    if (e == cudaSuccess && ln.mode == 3 && ln.nred > 0) {
+      e = launch_col_reduce(c->tab,
+                            reinterpret_cast<const ColReduceTask*>(c->ws + c->P.off_red) + ln.red_off,
+                            ln.nred, ln.nitems, s);
+      ++c->launches;
+    }
+  }
   else if (parity == 0)
     e = launch_row(0, c->P.RT, c->tab, dev_rowsegs(c, ln), dev_ctab(c, ln), ln.ncta, 1.0f, ef, s);
   else
@@ -743,7 +785,8 @@ acp_status acp_create(const acp_config* cfg, acp_ctx** out) {
       (e = up(P.off_streamsegs, P.streamsegs.data(), sizeof(StreamSeg) * P.streamsegs.size())) != cudaSuccess ||
       (e = up(P.off_orth[0], P.orthsegs[0].data(), sizeof(OrthSeg) * P.orthsegs[0].size())) != cudaSuccess ||
       (e = up(P.off_orth[1], P.orthsegs[1].data(), sizeof(OrthSeg) * P.orthsegs[1].size())) != cudaSuccess ||
-      (e = up(P.off_ctab, P.ctab.data(), 4 * P.ctab.size())) != cudaSuccess)
+      (e = up(P.off_ctab, P.ctab.data(), 4 * P.ctab.size())) != cudaSuccess ||
+      (e = up(P.off_red, P.redtasks.data(), sizeof(ColReduceTask) * P.redtasks.size())) != cudaSuccess)
     return bail(e, "plan upload");
   // Q_0: caller-provided (row-major m x r per matrix) or generated
   std::vector<float> q0;
@@ -769,7 +812,7 @@ acp_status acp_create(const acp_config* cfg, acp_ctx** out) {
   if (cfg->world_size > 1) {
     if ((e = cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking)) != cudaSuccess)
       return bail(e, "comm stream");
-    const size_t nb = std::max(P.buckets[0].size(), P.buckets[1].size());
+    const size_t nb = std::max(P.groups[0].size(), P.groups[1].size());
     c->ev_k1.resize(nb);
     c->ev_ar.resize(nb);
     for (size_t b = 0; b < nb; ++b) {
@@ -798,25 +841,31 @@ acp_status enqueue_step(acp_ctx* c, int32_t parity, cudaStream_t s) {
     return ACP_OK;
   }
   float* buf = parity == 0 ? c->tab.pbuf : c->tab.qbuf;
-  const size_t nb = P.buckets[parity].size();
-  for (size_t b = 0; b < nb; ++b) {
-    if ((st = run_k1(c, parity, P.k1_b[parity][b], s)) != ACP_OK) return st;
-    CK(c, cudaEventRecord(c->ev_k1[b], s), "event record");
-    CK(c, cudaStreamWaitEvent(c->comm_stream, c->ev_k1[b], 0), "stream wait");
-    ProfRec* r = prof_begin(c, ACP_K_ALLREDUCE, 4.0 * P.bcnt[parity][b], c->comm_stream);
-    ncclResult_t nr = ncclAllReduce(buf + P.boff[parity][b], buf + P.boff[parity][b],
-                                    (size_t)P.bcnt[parity][b], ncclFloat, ncclSum, c->comm,
-                                    c->comm_stream);
+  const size_t ng = P.groups[parity].size();
+  for (size_t g = 0; g < ng; ++g) {
+    if ((st = run_k1(c, parity, P.k1_g[parity][g], s)) != ACP_OK) return st;
+    CK(c, cudaEventRecord(c->ev_k1[g], s), "event record");
+    CK(c, cudaStreamWaitEvent(c->comm_stream, c->ev_k1[g], 0), "stream wait");
+    const int b0 = P.groups[parity][g].first, b1 = P.groups[parity][g].second;
+    double bytes = 0;
+    for (int b = b0; b <= b1; ++b) bytes += 4.0 * P.bcnt[parity][b];
+    ProfRec* r = prof_begin(c, ACP_K_ALLREDUCE, bytes, c->comm_stream);
+    ncclResult_t nr = ncclGroupStart();
+    for (int b = b0; b <= b1 && nr == ncclSuccess; ++b)
+      nr = ncclAllReduce(buf + P.boff[parity][b], buf + P.boff[parity][b],
+                         (size_t)P.bcnt[parity][b], ncclFloat, ncclSum, c->comm, c->comm_stream);
+    const ncclResult_t ne = ncclGroupEnd();
+    if (nr == ncclSuccess) nr = ne;
     prof_end(r, c->comm_stream);
     if (nr != ncclSuccess) {
       c->poisoned = true;
       return fail(ACP_E_NCCL, std::string("ncclAllReduce: ") + ncclGetErrorString(nr));
     }
-    CK(c, cudaEventRecord(c->ev_ar[b], c->comm_stream), "event record");
+    CK(c, cudaEventRecord(c->ev_ar[g], c->comm_stream), "event record");
   }
-  for (size_t b = 0; b < nb; ++b) {
-    CK(c, cudaStreamWaitEvent(s, c->ev_ar[b], 0), "stream wait");
-    if ((st = run_k3(c, parity, P.k3_b[parity][b], s)) != ACP_OK) return st;
+  for (size_t g = 0; g < ng; ++g) {
+    CK(c, cudaStreamWaitEvent(s, c->ev_ar[g], 0), "stream wait");
+    if ((st = run_k3(c, parity, P.k3_g[parity][g], s)) != ACP_OK) return st;
   }
   return ACP_OK;
 }

@@ -115,6 +115,7 @@ struct Shared {
   uint64_t* empty;
   float* red;    // [2][16 warps][8] row-group partial sums
   float* gred;   // generic path block reduction [16][32]
+  float4* cred;  // column mode: cross-row-slot combine [NW*32]
   int* flag;
   int stage_floats;
   int stages;
@@ -361,15 +362,25 @@ __device__ void seg_fast(const Tables& t, const LayerDesc& L, const StreamSeg& s
     pp.advance(sh.stages);
   }
   if constexpr (MODE == 3) {
-    // partial slot `rowslot` of this segment: k-major [r][pc], 16-byte stride
-    const int64_t stride = ((int64_t)r * pc + 3) & ~int64_t(3);
-    float* part = t.colpart + s.part_off + (int64_t)rowslot * stride;
+    // combine the row slots of the CTA (fixed order) and write ONE partial
+    // slot for this segment: k-major [r][pc], stride round4(r * pc)
+    float* part = t.colpart + s.part_off;
+    const int rpw = 32 / lg;  // row slots per warp
 #pragma unroll
     for (int i = 0; i < NC; ++i) {
-      if (cval[i]) {
 #pragma unroll
-        for (int k = 0; k < RT; ++k)
-          if (k < r) *reinterpret_cast<float4*>(part + (int64_t)k * pc + coff[i]) = acc3[i][k];
+      for (int k = 0; k < RT; ++k) {
+        cta_sync1<NW * 32>();
+        sh.cred[threadIdx.x] = acc3[i][k];
+        cta_sync1<NW * 32>();
+        if (rowslot == 0 && cval[i] && k < r) {
+          float4 sum = acc3[i][k];
+          for (int j = 1; j < NRS; ++j) {
+            const int w = (j / rpw) * gw + sub, ln = (j % rpw) * lg + li;
+            sum = f4add(sum, sh.cred[w * 32 + ln]);
+          }
+          *reinterpret_cast<float4*>(part + (int64_t)k * pc + coff[i]) = sum;
+        }
       }
     }
   }
@@ -417,7 +428,6 @@ __device__ void seg_generic(const Tables& t, const LayerDesc& L, const StreamSeg
   const int64_t c1 = (c0 + pc) < m ? (c0 + pc) : m;
   if constexpr (MODE == 3) {
     float* part = t.colpart + s.part_off;
-    const int64_t stride = ((int64_t)r * pc + 3) & ~int64_t(3);
     for (int64_t cb = c0; cb < c1; cb += NT) {
       const int64_t c = cb + threadIdx.x;
       if (c < c1) {
@@ -433,8 +443,6 @@ __device__ void seg_generic(const Tables& t, const LayerDesc& L, const StreamSeg
 #pragma unroll
         for (int k = 0; k < RT; ++k)
           if (k < r) part[k * pc + (c - c0)] = acc[k];
-        for (int gsl = 1; gsl < s.nslot; ++gsl)
-          for (int k = 0; k < r; ++k) part[(int64_t)gsl * stride + k * pc + (c - c0)] = 0.f;
       }
     }
     return;
@@ -485,40 +493,6 @@ __device__ void seg_generic(const Tables& t, const LayerDesc& L, const StreamSeg
   }
 }
 
-// last segment of a layer to finish (mode 3): sum the layer's partial slots in
-// slot order into the Q-buffer slot and the local-Q copy (deterministic)
-template <int NT>
-__device__ void col_finish(const Tables& t, const LayerDesc& L, const StreamSeg& s, int* flag) {
-  __threadfence();
-  cta_sync1<NT>();
-  if (threadIdx.x == 0) {
-    const int old = atomicAdd(t.colcnt + s.counter, s.nslot);
-    *flag = (old + s.nslot == s.pcount);
-  }
-  cta_sync1<NT>();
-  if (!*flag) return;
-  __threadfence();
-  const int64_t m = L.m;
-  const int r = L.r;
-  const StreamMap mp = L.sm[2];
-  const int64_t pc = mp.tr > 0 ? mp.pcols : m;   // generic layers: one full-width panel
-  const int64_t c0 = (int64_t)s.panel * pc;
-  const int64_t cols = (m - c0) < pc ? (m - c0) : pc;
-  const int64_t slot = ((int64_t)r * pc + 3) & ~int64_t(3);
-  const float* first = t.colpart + s.part_off - (int64_t)s.pidx * slot;
-  float* Qs = t.qbuf + L.q_off + c0;
-  float* Ql = t.qloc + L.ql_off + c0;
-  const int64_t total = (int64_t)r * cols;
-  for (int64_t i = threadIdx.x; i < total; i += NT) {
-    const int64_t k = i / cols, j = i - k * cols;
-    float acc = __ldcg(first + k * pc + j);
-    for (int p = 1; p < s.pcount; ++p) acc += __ldcg(first + p * slot + k * pc + j);
-    Qs[k * m + j] = acc;
-    Ql[k * m + j] = acc;
-  }
-  if (threadIdx.x == 0) t.colcnt[s.counter] = 0;  // re-arm
-}
-
 template <int MODE, int RT>
 __global__ void __launch_bounds__(Cfg<MODE>::NW * 32 + 32, Cfg<MODE>::CPS)
     stream_kernel(Tables t, const StreamSeg* __restrict__ segs, const int32_t* __restrict__ cta_begin,
@@ -534,7 +508,8 @@ __global__ void __launch_bounds__(Cfg<MODE>::NW * 32 + 32, Cfg<MODE>::CPS)
   sh.empty = sh.full + stages;
   sh.red = reinterpret_cast<float*>(sh.empty + stages);
   sh.gred = sh.red + 2 * 16 * 8;
-  sh.flag = reinterpret_cast<int*>(sh.gred + 16 * 32);
+  sh.cred = reinterpret_cast<float4*>(sh.gred + 16 * 32);
+  sh.flag = reinterpret_cast<int*>(sh.cred + 16 * 32);
   if (threadIdx.x == 0) {
     for (int i = 0; i < stages; ++i) {
       mbar_init(&sh.full[i], 1);
@@ -585,7 +560,6 @@ __global__ void __launch_bounds__(Cfg<MODE>::NW * 32 + 32, Cfg<MODE>::CPS)
         default: break;
       }
     }
-    if constexpr (MODE == 3) col_finish<NT>(t, L, s, sh.flag);
   }
 }
 
@@ -608,7 +582,70 @@ cudaError_t launch_mode(int rt, const Tables& t, const StreamSeg* segs, const in
   }
 }
 
+// K1 Q-step, second stage: Q_loc of each (layer, panel) = sum of its
+// segments' partial slots, in slot order (deterministic). 8 lanes share one
+// output float4 (each sums every 8th slot), combined by a fixed shuffle tree.
+__global__ void __launch_bounds__(256) col_reduce_kernel(Tables t, const ColReduceTask* __restrict__ tasks,
+                                                        int ntasks) {
+  constexpr int kSplit = 8;
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int item = gtid / kSplit, j = gtid % kSplit;
+  // items are laid out task by task: item -> (task, k, float4 column)
+  int lo = 0, hi = ntasks - 1;
+  if (item >= tasks[ntasks - 1].item_end) return;
+  while (lo < hi) {  // first task whose item_end > item
+    const int mid = (lo + hi) >> 1;
+    if (tasks[mid].item_end > item) hi = mid; else lo = mid + 1;
+  }
+  const ColReduceTask tk = tasks[lo];
+  const int local = item - tk.item_begin;
+  const int c4 = (int)((tk.cols + 3) / 4);
+  const int k = local / c4, c = (local - k * c4) * 4;
+  const float* base = t.colpart + tk.part_first + (int64_t)k * tk.pc + c;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  const bool vec = (tk.cols & 3) == 0;
+  for (int p = j; p < tk.pcount; p += kSplit) {
+    const float* src = base + (int64_t)p * tk.stride;
+    if (vec) {
+      acc = f4add(acc, __ldcg(reinterpret_cast<const float4*>(src)));
+    } else {
+      acc.x += __ldcg(src);
+      if (c + 1 < tk.cols) acc.y += __ldcg(src + 1);
+      if (c + 2 < tk.cols) acc.z += __ldcg(src + 2);
+      if (c + 3 < tk.cols) acc.w += __ldcg(src + 3);
+    }
+  }
+#pragma unroll
+  for (int off = 1; off < kSplit; off <<= 1) {
+    acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
+    acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
+    acc.z += __shfl_xor_sync(0xffffffffu, acc.z, off);
+    acc.w += __shfl_xor_sync(0xffffffffu, acc.w, off);
+  }
+  if (j != 0) return;
+  float* q = t.qbuf + tk.q_dst + (int64_t)k * tk.m + c;
+  float* ql = t.qloc + tk.ql_dst + (int64_t)k * tk.m + c;
+  if (vec) {
+    *reinterpret_cast<float4*>(q) = acc;
+    *reinterpret_cast<float4*>(ql) = acc;
+  } else {
+    const float v[4] = {acc.x, acc.y, acc.z, acc.w};
+    for (int u = 0; u < 4 && c + u < tk.cols; ++u) {
+      q[u] = v[u];
+      ql[u] = v[u];
+    }
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_col_reduce(const Tables& t, const ColReduceTask* tasks, int ntasks, int nitems,
+                              cudaStream_t s) {
+  if (ntasks <= 0 || nitems <= 0) return cudaSuccess;
+  const int64_t threads = (int64_t)nitems * 8;
+  col_reduce_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(t, tasks, ntasks);
+  return cudaGetLastError();
+}
 
 cudaError_t allow_max_smem(const void* kern) {
   // one attribute call per (kernel, device); the table is tiny and process-wide
@@ -625,7 +662,8 @@ cudaError_t allow_max_smem(const void* kern) {
 }
 
 size_t stream_smem_bytes(int stages, int stage_floats) {
-  return (size_t)2 * stages * stage_floats * 4 + 2 * stages * 8 + (2 * 16 * 8 + 16 * 32) * 4 + 16;
+  return (size_t)2 * stages * stage_floats * 4 + 2 * stages * 8 + (2 * 16 * 8 + 16 * 32) * 4 +
+         16 * 32 * 16 + 16;
 }
 
 // Host: choose the thread mapping of an m-column layer for stream mode
