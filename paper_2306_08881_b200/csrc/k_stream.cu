@@ -189,6 +189,125 @@ __device__ void producer(const Tables& t, const StreamSeg* segs, int sb, int se,
 }
 
 // ---------------------------------------------------------------------------
+// K1 P-step, bulk-pipelined, lean consumer loop (~14 thread-instructions per
+// element at r = 4): invalid chunks / rows read a valid (clamped) shared
+// address and contribute 0 through zero factor registers or are simply not
+// stored, so the loop has no data-dependent selects; dot products accumulate
+// straight into the row sums with FMAs; whole-warp rows use an unconditional
+// 5-level butterfly; rows spread over gw warps are combined by RT lanes
+// after one named barrier and broadcast with RT shuffles.
+// ---------------------------------------------------------------------------
+template <int RT, int NC>
+__device__ void seg_k1p(const Tables& t, const LayerDesc& L, const StreamSeg& s,
+                        const Shared& sh, Pipe& pp, int& rph) {
+  constexpr int NW = Cfg<0>::NW;
+  const StreamMap mp = L.sm[0];
+  const int lg = mp.lg, gw = mp.gw, rs = mp.rs, TR = mp.tr;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int sub = warp % gw, wrow = warp / gw;
+  const int lgi = lane / lg, li = lane - lgi * lg;
+  const int rowslot = wrow * (32 / lg) + lgi;
+  const int NRS = (NW / gw) * (32 / lg);
+  const int m = (int)L.m;
+  const int n = (int)L.n;
+  const int r = L.r;
+  const int m4 = m >> 2;
+  const int cbase = sub * lg * NC + li;
+  int coff[NC];
+  bool cval[NC];
+#pragma unroll
+  for (int i = 0; i < NC; ++i) {
+    const int c = cbase + lg * i;
+    cval[i] = c < m4;
+    coff[i] = 4 * (cval[i] ? c : 0);
+  }
+  float4 qa[NC][RT];
+  {
+    const float* Qf = t.qbuf + L.q_off;
+#pragma unroll
+    for (int i = 0; i < NC; ++i)
+#pragma unroll
+      for (int k = 0; k < RT; ++k) qa[i][k] = (cval[i] && k < r) ? ld_f4(Qf + k * m + coff[i]) : zero4();
+  }
+  float* __restrict__ E = t.E + L.e_off;
+  float* __restrict__ Pw = t.pbuf + L.p_off;
+  const bool pwriter = (sub == 0) && (li == 0);
+  for (int64_t r0 = s.row0; r0 < s.row1; r0 += TR) {
+    const int nr = (int)((s.row1 - r0) < TR ? (s.row1 - r0) : TR);
+    const int stage = pp.stage;
+    mbar_wait(&sh.full[stage], pp.phase);
+    const float* tM = sh.sM + (size_t)stage * sh.stage_floats;
+    const float* tE = sh.sE + (size_t)stage * sh.stage_floats;
+    for (int j = 0; j < rs; ++j) {
+      const int tri = rowslot + NRS * j;
+      const bool rval = tri < nr;
+      const int toff = (rval ? tri : 0) * m;
+      float4 x[NC];
+#pragma unroll
+      for (int i = 0; i < NC; ++i) x[i] = f4add(lds4(tM + toff + coff[i]), lds4(tE + toff + coff[i]));
+      if (j == rs - 1) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sh.empty[stage]);
+      }
+      float acc[RT];
+#pragma unroll
+      for (int k = 0; k < RT; ++k) {
+        float a = 0.f;
+#pragma unroll
+        for (int i = 0; i < NC; ++i) {
+          a = fmaf(x[i].x, qa[i][k].x, a);
+          a = fmaf(x[i].y, qa[i][k].y, a);
+          a = fmaf(x[i].z, qa[i][k].z, a);
+          a = fmaf(x[i].w, qa[i][k].w, a);
+        }
+        acc[k] = a;
+      }
+      if (lg == 32) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+          for (int k = 0; k < RT; ++k) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], off);
+      } else {
+        for (int off = lg >> 1; off > 0; off >>= 1)
+#pragma unroll
+          for (int k = 0; k < RT; ++k) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], off);
+      }
+      if (gw > 1) {
+        float* buf = sh.red + (rph & 1) * (16 * 8);
+        ++rph;
+        float mine = acc[0];
+#pragma unroll
+        for (int k = 1; k < RT; ++k)
+          if (lane == k) mine = acc[k];
+        if (lane < RT) buf[warp * 8 + lane] = mine;
+        cta_sync1<NW * 32>();
+        float tot = 0.f;
+        if (lane < RT) {
+          const float* gb = buf + (wrow * gw) * 8 + lane;
+          for (int w = 0; w < gw; ++w) tot += gb[w * 8];
+        }
+#pragma unroll
+        for (int k = 0; k < RT; ++k) acc[k] = __shfl_sync(0xffffffffu, tot, k);
+      }
+      const int64_t row = r0 + tri;
+#pragma unroll
+      for (int i = 0; i < NC; ++i) {
+        float4 e = x[i];
+#pragma unroll
+        for (int k = 0; k < RT; ++k) f4fma(e, -acc[k], qa[i][k]);
+        if (rval && cval[i]) st_cs4(E + row * m + coff[i], e);
+      }
+      if (rval && pwriter) {
+#pragma unroll
+        for (int k = 0; k < RT; ++k)
+          if (k < r) Pw[(int64_t)k * n + row] = acc[k];
+      }
+    }
+    pp.advance(sh.stages);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // fast (bulk-pipelined) segment
 // ---------------------------------------------------------------------------
 template <int MODE, int RT, int NC>
@@ -548,8 +667,10 @@ __global__ void __launch_bounds__(Cfg<MODE>::NW * 32 + 32, Cfg<MODE>::CPS)
       switch (L.sm[ModeIdx<MODE>::v].nc) {
 #define ACP_CASE(NCV)                                                            \
   case NCV:                                                                      \
-    if constexpr (NCV <= nc_max(MODE, RT))                                       \
-      seg_fast<MODE, RT, NCV>(t, L, s, grad, scale, sh, pp, rph);                  \
+    if constexpr (NCV <= nc_max(MODE, RT)) {                                     \
+      if constexpr (MODE == 0) seg_k1p<RT, NCV>(t, L, s, sh, pp, rph);           \
+      else seg_fast<MODE, RT, NCV>(t, L, s, grad, scale, sh, pp, rph);          \
+    }                                                                            \
     break;
         ACP_CASE(1)
         ACP_CASE(2)
