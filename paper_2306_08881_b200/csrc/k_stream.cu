@@ -44,7 +44,7 @@ template <> struct Cfg<2> { static constexpr int NW = 8, CPS = 1, TT = 4096; };
 template <> struct Cfg<3> { static constexpr int NW = 8, CPS = 1, TT = 8192; };
 
 __host__ __device__ constexpr int nc_max(int mode, int RT) {
-  return mode == 0 ? (RT <= 4 ? 5 : (RT == 8 ? 2 : 0))
+  return mode == 0 ? (RT <= 4 ? 5 : (RT == 8 ? 4 : 0))
                    : (mode == 2 ? (RT <= 4 ? 3 : (RT == 8 ? 1 : 0)) : (RT <= 4 ? 4 : (RT == 8 ? 2 : 0)));
 }
 
@@ -242,25 +242,28 @@ __device__ void seg_k1p(const Tables& t, const LayerDesc& L, const StreamSeg& s,
       const int tri = rowslot + NRS * j;
       const bool rval = tri < nr;
       const int toff = (rval ? tri : 0) * m;
-      float4 x[NC];
-#pragma unroll
-      for (int i = 0; i < NC; ++i) x[i] = f4add(lds4(tM + toff + coff[i]), lds4(tE + toff + coff[i]));
-      if (j == rs - 1) {
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sh.empty[stage]);
-      }
+      // RT >= 8: x is re-read from shared memory for the residual (registers
+      // go to the factor); the stage is then released after the residual
+      constexpr bool kReload = RT >= 8;
+      float4 x[kReload ? 1 : NC];
       float acc[RT];
 #pragma unroll
-      for (int k = 0; k < RT; ++k) {
-        float a = 0.f;
+      for (int k = 0; k < RT; ++k) acc[k] = 0.f;
 #pragma unroll
-        for (int i = 0; i < NC; ++i) {
-          a = fmaf(x[i].x, qa[i][k].x, a);
-          a = fmaf(x[i].y, qa[i][k].y, a);
-          a = fmaf(x[i].z, qa[i][k].z, a);
-          a = fmaf(x[i].w, qa[i][k].w, a);
+      for (int i = 0; i < NC; ++i) {
+        const float4 xi = f4add(lds4(tM + toff + coff[i]), lds4(tE + toff + coff[i]));
+        if constexpr (!kReload) x[i] = xi;
+#pragma unroll
+        for (int k = 0; k < RT; ++k) {
+          acc[k] = fmaf(xi.x, qa[i][k].x, acc[k]);
+          acc[k] = fmaf(xi.y, qa[i][k].y, acc[k]);
+          acc[k] = fmaf(xi.z, qa[i][k].z, acc[k]);
+          acc[k] = fmaf(xi.w, qa[i][k].w, acc[k]);
         }
-        acc[k] = a;
+      }
+      if (!kReload && j == rs - 1) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sh.empty[stage]);
       }
       if (lg == 32) {
 #pragma unroll
@@ -292,10 +295,16 @@ __device__ void seg_k1p(const Tables& t, const LayerDesc& L, const StreamSeg& s,
       const int64_t row = r0 + tri;
 #pragma unroll
       for (int i = 0; i < NC; ++i) {
-        float4 e = x[i];
+        float4 e;
+        if constexpr (kReload) e = f4add(lds4(tM + toff + coff[i]), lds4(tE + toff + coff[i]));
+        else e = x[i];
 #pragma unroll
         for (int k = 0; k < RT; ++k) f4fma(e, -acc[k], qa[i][k]);
         if (rval && cval[i]) st_cs4(E + row * m + coff[i], e);
+      }
+      if (kReload && j == rs - 1) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sh.empty[stage]);
       }
       if (rval && pwriter) {
 #pragma unroll
