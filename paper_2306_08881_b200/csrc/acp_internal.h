@@ -124,12 +124,16 @@ struct Tables {
   int32_t* orthcnt;
   uint32_t* degmask;
   int64_t* step;         // device step counter (keys the method's random draws)
+  int32_t* deferred;     // 1: E holds S = M' of the last Q-step (E = S - P Q_loc^T
+                         //    is applied lazily by the next P-step), 0: E is materialised
 };
 
 // launches (all on `stream`, 256 threads, grid = ncta)
 // mode 0: K1 P-step (projection + residual + pack into P-buffer)
 // mode 1: K3 P-step decode (+ unpack from P-buffer)
 // mode 2: K3 Q-step residual + decode (+ unpack from Q-buffer)
+// mode 3: K3 Q-step decode only, deferred residual (+ unpack from Q-buffer)
+// (mode 1 also clears *t.deferred: the P-step's K1 has consumed it)
 cudaError_t launch_row(int mode, int rt, const Tables& t, const RowSeg* segs,
                        const int32_t* cta_begin, int ncta, float scale, int ef,
                        cudaStream_t stream);
@@ -142,12 +146,19 @@ cudaError_t launch_col_reduce(const Tables& t, const ColReduceTask* tasks, int n
                               cudaStream_t stream);
 // Raise the dynamic shared-memory limit of a kernel once per device.
 cudaError_t allow_max_smem(const void* kern);
+// defer = 1 (deferred Q-step residual): mode 3 also writes
+// S = M + E back into E and raises *t.deferred; mode 0 applies
+// E_prev = S - P Q_loc^T on the fly when *t.deferred is set (Q_loc staged in
+// factor_floats of shared memory).
 cudaError_t launch_stream(int mode, int rt, const Tables& t, const StreamSeg* segs,
                           const int32_t* cta_begin, int ncta, float scale, int stages,
-                          int stage_floats, cudaStream_t stream);
+                          int stage_floats, int factor_floats, int defer, cudaStream_t stream);
+// E (or dst) = S - P Q_loc^T for one matrix layer (deferred state -> E)
+cudaError_t launch_materialize(const Tables& t, const LayerDesc& L, int layer, float* dst,
+                               cudaStream_t stream);
 bool stream_make_map(int mode, int64_t m, int rt, StreamMap* out);
 int stream_ctas_per_sm(int mode);
-size_t stream_smem_bytes(int stages, int stage_floats);
+size_t stream_smem_bytes(int stages, int stage_floats, int factor_floats);
 // K2: CholeskyQR2 of the factors named by segs (side 0: Q factors in the
 // Q-buffer, length m; side 1: P factors in the P-buffer, length n).
 cudaError_t launch_orth(int rt, const Tables& t, int side, const OrthSeg* segs, int nseg,

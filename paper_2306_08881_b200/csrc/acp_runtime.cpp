@@ -41,7 +41,7 @@ struct Launch {
   int64_t seg_off = 0;   // first segment (row, col or stream array)
   int64_t cb_off = 0;    // first entry of cta_begin
   int ncta = 0;
-  int stages = 0, stage_floats = 0;
+  int stages = 0, stage_floats = 0, factor_floats = 0, defer = 0;
   int64_t red_off = 0;   // K1 Q-step: first ColReduceTask of this launch
   int nred = 0, nitems = 0;
   double bytes = 0;      // algorithmic bytes moved by this launch
@@ -58,6 +58,7 @@ struct Unit {
 struct Plan {
   int T = 0, RT = 1, nsm = 148, nmat = 0;
   bool ef = true;
+  bool defer = false;   // deferred Q-step residual (stream kernels)
   std::vector<LayerDesc> L;
   int64_t N = 0, e_elems = 0, arena[2] = {0, 0}, ql_elems = 0, wmat_elems = 0;
   std::vector<std::vector<int>> buckets[2];
@@ -83,7 +84,7 @@ struct Plan {
   size_t off_E = 0, off_P = 0, off_Q = 0, off_QL = 0, off_colpart = 0, off_colcnt = 0,
          off_gram = 0, off_wmat = 0, off_orthcnt = 0, off_degmask = 0, off_layers = 0,
          off_grads = 0, off_rowsegs = 0, off_colsegs = 0, off_streamsegs = 0, off_orth[2] = {0, 0},
-         off_ctab = 0, off_step = 0, off_red = 0,
+         off_ctab = 0, off_step = 0, off_red = 0, off_defer = 0,
          total = 0;
 };
 
@@ -258,14 +259,14 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
         bytes += 8.0 * L.n;
         continue;
       }
-      const double bpe = mode == 0 ? (ef ? 12.0 : 4.0) : (mode == 1 ? 4.0 : (ef ? 16.0 : 8.0));
+      const double bpe = mode == 0 ? (ef ? 12.0 : 4.0) : ((mode == 1 || mode == 3) ? 4.0 : (ef ? 16.0 : 8.0));
       int64_t align = 1;
       if (L.G > 0) align = (int64_t)(kThreads / L.G) * row_rows_per_iter(mode, L.V, P.RT);
       units.push_back({i, -1, L.n, bpe * (double)L.m, align});
       // algorithmic bytes: M/E stream + factor traffic (each factor touched once)
       bytes += bpe * (double)L.n * (double)L.m;
       if (mode == 0) bytes += 4.0 * L.r * (double)(L.m + L.n);
-      if (mode == 1) bytes += 4.0 * L.r * (double)(L.m + L.n);
+      if (mode == 1 || mode == 3) bytes += 4.0 * L.r * (double)(L.m + L.n);
       if (mode == 2) bytes += 4.0 * L.r * (double)(2 * L.m + L.n);
     }
     Launch ln;
@@ -351,7 +352,7 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
     const int mi = mode == 0 ? 0 : (mode == 2 ? 1 : 2);
     std::vector<Unit> units;
     double bytes = 0;
-    int64_t stage_floats = 32;
+    int64_t stage_floats = 32, factor_floats = 0;
     for (int i : tensors) {
       const LayerDesc& L = P.L[i];
       if (!L.mat) {
@@ -359,13 +360,15 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
         bytes += 8.0 * L.n;
         continue;
       }
-      const double bpe = mode == 0 ? 12.0 : (mode == 2 ? 16.0 : 8.0);
+      const double bpe = mode == 0 ? 12.0 : (mode == 2 ? 16.0 : (P.defer ? 12.0 : 8.0));
       const StreamMap& mp = L.sm[mi];
       const bool fast = mp.tr > 0;
       const int64_t tr = fast ? mp.tr : 1;
       const int64_t pc = fast ? mp.pcols : L.m;
       const int np = fast ? mp.np : 1;
       if (fast) stage_floats = std::max<int64_t>(stage_floats, tr * pc);
+      if (fast && mode == 0 && P.defer)  // staged Q_loc [RT][m]
+        factor_floats = std::max<int64_t>(factor_floats, (int64_t)P.RT * L.m);
       for (int pn = 0; pn < np; ++pn) {
         const int64_t cols = std::min<int64_t>(pc, L.m - (int64_t)pn * pc);
         units.push_back({i, pn, L.n, bpe * (double)cols, tr});
@@ -382,10 +385,12 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
     ln.cb_off = (int64_t)P.ctab.size();
     stage_floats = (stage_floats + 31) / 32 * 32;
     const int cps = stream_ctas_per_sm(mode);
-    const int64_t budget = (cps == 1 ? 200 : 96) * 1024;
+    const int64_t budget = (cps == 1 ? 200 : 96) * 1024 - 4 * factor_floats;
     int stages = (int)std::min<int64_t>(8, budget / (2 * 4 * stage_floats));
     ln.stages = std::max(2, stages);
     ln.stage_floats = (int)stage_floats;
+    ln.factor_floats = (int)factor_floats;
+    ln.defer = (P.defer && (mode == 0 || mode == 3)) ? 1 : 0;
     int64_t part = 0;
     int prev_layer = -1, prev_panel = -1;
     ln.red_off = (int64_t)P.redtasks.size();
@@ -432,11 +437,15 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
     return ln;
   };
   const bool use_stream = P.ef && P.RT <= 8;
+  // the deferred Q-step residual needs the stream kernels' layouts; the
+  // environment switch keeps the 24-B/element Q-step for comparison
+  P.defer = use_stream && !std::getenv("ACP_NO_DEFER");
   auto k1_launch = [&](int parity, const std::vector<int>& ts) {
     if (use_stream) return stream_launch(parity == 0 ? 0 : 3, ts);
     return parity == 0 ? row_launch(0, ts) : col_launch(ts);
   };
   auto k3_launch = [&](int parity, const std::vector<int>& ts) {
+    if (parity == 1 && P.defer) return row_launch(3, ts);  // decode only
     if (parity == 1 && use_stream) return stream_launch(2, ts);
     return row_launch(parity == 0 ? 1 : 2, ts);
   };
@@ -529,6 +538,7 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
   P.off_orth[1] = take(sizeof(OrthSeg) * P.orthsegs[1].size());
   P.off_ctab = take(4 * P.ctab.size());
   P.off_step = take(8);
+  P.off_defer = take(8);
   P.off_red = take(sizeof(ColReduceTask) * P.redtasks.size());
   P.total = o;
   return ACP_OK;
@@ -564,6 +574,7 @@ struct acp_ctx {
   std::vector<cudaEvent_t> ev_k1, ev_ar;
   std::vector<float*> grads_cache;
   int64_t step_count = 0;
+  bool e_deferred = false;  // host mirror of *tab.deferred
   int64_t launches = 0;
   bool poisoned = false;
   bool profile = false;
@@ -633,7 +644,7 @@ acp_status run_k1(acp_ctx* c, int parity, const Launch& ln, cudaStream_t s) {
   cudaError_t e;
   if (ln.kind == 2) {
     e = launch_stream(ln.mode, c->P.RT, c->tab, dev_streamsegs(c, ln), dev_ctab(c, ln), ln.ncta,
-                      1.0f, ln.stages, ln.stage_floats, s);
+                      1.0f, ln.stages, ln.stage_floats, ln.factor_floats, ln.defer, s);
     if (e == cudaSuccess && ln.mode == 3 && ln.nred > 0) {
       e = launch_col_reduce(c->tab,
                             reinterpret_cast<const ColReduceTask*>(c->ws + c->P.off_red) + ln.red_off,
@@ -658,8 +669,8 @@ acp_status run_k3(acp_ctx* c, int parity, const Launch& ln, cudaStream_t s) {
   cudaError_t e =
       ln.kind == 2
           ? launch_stream(ln.mode, c->P.RT, c->tab, dev_streamsegs(c, ln), dev_ctab(c, ln), ln.ncta,
-                          decode_scale(c), ln.stages, ln.stage_floats, s)
-          : launch_row(parity == 0 ? 1 : 2, c->P.RT, c->tab, dev_rowsegs(c, ln), dev_ctab(c, ln),
+                          decode_scale(c), ln.stages, ln.stage_floats, ln.factor_floats, ln.defer, s)
+          : launch_row(ln.mode, c->P.RT, c->tab, dev_rowsegs(c, ln), dev_ctab(c, ln),
                        ln.ncta, decode_scale(c), ef, s);
   prof_end(r, s);
   if (e != cudaSuccess) return cuda_fail(c, e, "decode kernel launch");
@@ -765,6 +776,7 @@ acp_status acp_create(const acp_config* cfg, acp_ctx** out) {
   t.orthcnt = reinterpret_cast<int32_t*>(c->ws + P.off_orthcnt);
   t.degmask = reinterpret_cast<uint32_t*>(c->ws + P.off_degmask);
   t.step = reinterpret_cast<int64_t*>(c->ws + P.off_step);
+  t.deferred = reinterpret_cast<int32_t*>(c->ws + P.off_defer);
 
   DeviceGuard dg(cfg->device);
   cudaStream_t s = nullptr;
@@ -828,6 +840,25 @@ acp_status acp_create(const acp_config* cfg, acp_ctx** out) {
 }  // extern "C"
 
 namespace {
+
+// Deferred Q-step residual -> materialised E for every matrix (repeated
+// Q-steps, set_state); eager, on stream s.
+acp_status materialize_all(acp_ctx* c, cudaStream_t s) {
+  if (!c->e_deferred) return ACP_OK;
+  for (int i = 0; i < c->P.T; ++i)
+    if (c->P.L[i].mat)
+      CK(c, launch_materialize(c->tab, c->P.L[i], i, nullptr, s), "materialize E");
+  CK(c, cudaMemsetAsync(c->tab.deferred, 0, sizeof(int32_t), s), "clear deferred flag");
+  c->e_deferred = false;
+  return ACP_OK;
+}
+
+// host bookkeeping before/after a K1 of `parity`
+acp_status before_k1(acp_ctx* c, int32_t parity, cudaStream_t s) {
+  if (parity == 1 && c->e_deferred) return materialize_all(c, s);  // Q after Q
+  return ACP_OK;
+}
+void after_k1(acp_ctx* c, int32_t parity) { c->e_deferred = c->P.defer && parity == 1; }
 
 // Enqueue one whole step (orthogonalise, per-bucket projection + all-reduce,
 // decode) on stream s; used eagerly and for graph capture.
@@ -903,6 +934,7 @@ acp_status acp_step(acp_ctx* c, int32_t parity, float* const* grads, void* strea
   DeviceGuard dg(c->cfg.device);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if ((st = set_grads(c, grads, s)) != ACP_OK) return st;
+  if ((st = before_k1(c, parity, s)) != ACP_OK) return st;
   if (c->use_graphs && !c->profile) {
     if (!c->gexec[parity] && (st = capture_step(c, parity)) != ACP_OK) return st;
     CK(c, cudaGraphLaunch(c->gexec[parity], s), "graph launch");
@@ -910,6 +942,7 @@ acp_status acp_step(acp_ctx* c, int32_t parity, float* const* grads, void* strea
   } else if ((st = enqueue_step(c, parity, s)) != ACP_OK) {
     return st;
   }
+  after_k1(c, parity);
   ++c->step_count;
   return ACP_OK;
 }
@@ -929,8 +962,10 @@ acp_status acp_compress(acp_ctx* c, int32_t parity, float* const* grads, float**
   DeviceGuard dg(c->cfg.device);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if ((st = set_grads(c, grads, s)) != ACP_OK) return st;
+  if ((st = before_k1(c, parity, s)) != ACP_OK) return st;
   if ((st = run_orth(c, parity, s)) != ACP_OK) return st;
   if ((st = run_k1(c, parity, c->P.k1_all[parity], s)) != ACP_OK) return st;
+  after_k1(c, parity);
   *out_buffer = parity == 0 ? c->tab.pbuf : c->tab.qbuf;
   *out_count = c->P.arena[parity];
   ++c->step_count;
@@ -956,8 +991,13 @@ acp_status acp_get_state(acp_ctx* c, int32_t i, float* Pm, float* Qm, float* Em,
   const LayerDesc& L = c->P.L[i];
   if (Pm) CK(c, launch_transpose(c->tab.pbuf + L.p_off, Pm, L.n, L.r, 0, s), "state transpose");
   if (Qm) CK(c, launch_transpose(c->tab.qbuf + L.q_off, Qm, L.m, L.r, 0, s), "state transpose");
-  if (Em) CK(c, cudaMemcpyAsync(Em, c->tab.E + L.e_off, 4 * (size_t)(L.n * L.m),
-                               cudaMemcpyDeviceToDevice, s), "state copy");
+  if (Em) {
+    if (c->e_deferred)  // E = S - P Q_loc^T, formed on the fly (state unchanged)
+      CK(c, launch_materialize(c->tab, L, i, Em, s), "materialize E");
+    else
+      CK(c, cudaMemcpyAsync(Em, c->tab.E + L.e_off, 4 * (size_t)(L.n * L.m),
+                            cudaMemcpyDeviceToDevice, s), "state copy");
+  }
   return ACP_OK;
 }
 
@@ -969,6 +1009,7 @@ acp_status acp_set_state(acp_ctx* c, int32_t i, const float* Pm, const float* Qm
   DeviceGuard dg(c->cfg.device);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const LayerDesc& L = c->P.L[i];
+  if ((st = materialize_all(c, s)) != ACP_OK) return st;  // other layers keep their E
   if (Pm) CK(c, launch_transpose(Pm, c->tab.pbuf + L.p_off, L.n, L.r, 1, s), "state transpose");
   if (Qm) CK(c, launch_transpose(Qm, c->tab.qbuf + L.q_off, L.m, L.r, 1, s), "state transpose");
   if (Em) CK(c, cudaMemcpyAsync(c->tab.E + L.e_off, Em, 4 * (size_t)(L.n * L.m),

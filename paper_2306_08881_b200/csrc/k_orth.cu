@@ -213,6 +213,24 @@ __global__ void fill_kernel(Tables t, int side, uint64_t seed, int tag, int64_t 
   }
 }
 
+// deferred state -> E: dst = S - P Q_loc^T for one matrix layer
+__global__ void materialize_kernel(Tables t, int layer, float* dst) {
+  const LayerDesc L = t.layers[layer];
+  const int64_t n = L.n, m = L.m;
+  const int r = L.r;
+  const float* S = t.E + L.e_off;
+  const float* P = t.pbuf + L.p_off;
+  const float* Ql = t.qloc + L.ql_off;
+  if (!dst) dst = t.E + L.e_off;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n * m;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = idx / m, j = idx - i * m;
+    float x = S[idx];
+    for (int k = 0; k < r; ++k) x = fmaf(-P[k * n + i], Ql[k * m + j], x);
+    dst[idx] = x;
+  }
+}
+
 __global__ void transpose_kernel(const float* __restrict__ src, float* __restrict__ dst,
                                  int64_t rows, int r, int to_kmajor) {
   const int64_t total = rows * r;
@@ -270,6 +288,16 @@ cudaError_t launch_fill(const Tables& t, const LayerDesc* host_layers, int num_t
   dim3 grid((unsigned)bx, (unsigned)num_tensors);
   fill_kernel<<<grid, kThreads, 0, s>>>(t, side, seed, tag, step);
   if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_materialize(const Tables& t, const LayerDesc& L, int layer, float* dst,
+                               cudaStream_t s) {
+  const int64_t total = L.n * L.m;
+  if (!L.mat || total == 0) return cudaSuccess;
+  int64_t blocks = (total + kThreads - 1) / kThreads;
+  if (blocks > 8192) blocks = 8192;
+  materialize_kernel<<<(unsigned)blocks, kThreads, 0, s>>>(t, layer, dst);
   return cudaGetLastError();
 }
 

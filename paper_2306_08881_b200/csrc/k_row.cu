@@ -370,6 +370,9 @@ __global__ void __launch_bounds__(kThreads) row_kernel(Tables t, const RowSeg* _
   __shared__ __align__(16) float red[2 * 8 * kRedSlots];
   __shared__ __align__(16) float red_gen[8 * 32];
   int phase = 0;
+  // the P-step decode runs after the P-step projection consumed a deferred
+  // Q-step residual (k_stream.cu): E is materialised again
+  if (MODE == 1 && blockIdx.x == 0 && threadIdx.x == 0) *t.deferred = 0;
   const int sb = cta_begin[blockIdx.x], se = cta_begin[blockIdx.x + 1];
   for (int s = sb; s < se; ++s) {
     const RowSeg sg = segs[s];
@@ -377,7 +380,7 @@ __global__ void __launch_bounds__(kThreads) row_kernel(Tables t, const RowSeg* _
     float* grad = t.grads[sg.layer];
     if (!L.mat) {
       // vectors: pack (mode 0) into the P-buffer / unpack (modes 1, 2)
-      float* slot = (MODE == 2 ? t.qbuf + L.q_off : t.pbuf + L.p_off);
+      float* slot = (MODE >= 2 ? t.qbuf + L.q_off : t.pbuf + L.p_off);
       for (int64_t i = sg.row0 + threadIdx.x; i < sg.row1; i += kThreads) {
         if (MODE == 0) slot[i] = grad[i];
         else grad[i] = slot[i] * scale;
@@ -386,7 +389,7 @@ __global__ void __launch_bounds__(kThreads) row_kernel(Tables t, const RowSeg* _
     }
     const bool fast = L.G > 0 && ((reinterpret_cast<uintptr_t>(grad) & 15u) == 0);
     if (!fast) {
-      row_generic<MODE, RT>(t, L, grad, sg.row0, sg.row1, scale, ef, red_gen);
+      row_generic<MODE == 3 ? 1 : MODE, RT>(t, L, grad, sg.row0, sg.row1, scale, ef, red_gen);
       continue;
     }
     if constexpr (MODE == 0) {
@@ -400,7 +403,7 @@ __global__ void __launch_bounds__(kThreads) row_kernel(Tables t, const RowSeg* _
         case 7: k1p_fast<RT, 7>(t, L, grad, sg.row0, sg.row1, ef, red, phase); break;
         default: k1p_fast<RT, 8>(t, L, grad, sg.row0, sg.row1, ef, red, phase); break;
       }
-    } else if constexpr (MODE == 1) {
+    } else if constexpr (MODE == 1 || MODE == 3) {
       k3p_fast<RT>(t, L, grad, sg.row0, sg.row1, scale);
     } else {
       k3q_fast<RT>(t, L, grad, sg.row0, sg.row1, scale, ef);
@@ -428,7 +431,7 @@ cudaError_t launch_row_mode(int rt, const Tables& t, const RowSeg* segs, const i
 
 int row_rows_per_iter(int mode, int V, int rt) {
   if (mode == 0) return rows_k1p(V, rt);
-  if (mode == 1) return rows_k3p(rt);
+  if (mode == 1 || mode == 3) return rows_k3p(rt);
   return rows_k3q(rt);
 }
 
@@ -440,6 +443,7 @@ cudaError_t launch_row(int mode, int rt, const Tables& t, const RowSeg* segs,
     case 0: return launch_row_mode<0>(rt, t, segs, cta_begin, ncta, scale, ef, stream);
     case 1: return launch_row_mode<1>(rt, t, segs, cta_begin, ncta, scale, ef, stream);
     case 2: return launch_row_mode<2>(rt, t, segs, cta_begin, ncta, scale, ef, stream);
+    case 3: return launch_row_mode<3>(rt, t, segs, cta_begin, ncta, scale, ef, stream);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -116,6 +116,7 @@ struct Shared {
   float* red;    // [2][16 warps][8] row-group partial sums
   float* gred;   // generic path block reduction [16][32]
   float4* cred;  // column mode: cross-row-slot combine [NW*32]
+  float* sQl;    // K1-P deferred: local Q factor of the segment's layer [RT][m]
   int* flag;
   int stage_floats;
   int stages;
@@ -199,7 +200,7 @@ __device__ void producer(const Tables& t, const StreamSeg* segs, int sb, int se,
 // ---------------------------------------------------------------------------
 template <int RT, int NC>
 __device__ void seg_k1p(const Tables& t, const LayerDesc& L, const StreamSeg& s,
-                        const Shared& sh, Pipe& pp, int& rph) {
+                        const Shared& sh, Pipe& pp, int& rph, int defer) {
   constexpr int NW = Cfg<0>::NW;
   const StreamMap mp = L.sm[0];
   const int lg = mp.lg, gw = mp.gw, rs = mp.rs, TR = mp.tr;
@@ -232,6 +233,26 @@ __device__ void seg_k1p(const Tables& t, const LayerDesc& L, const StreamSeg& s,
   float* __restrict__ E = t.E + L.e_off;
   float* __restrict__ Pw = t.pbuf + L.p_off;
   const bool pwriter = (sub == 0) && (li == 0);
+  if (defer) {
+    // deferred Q-step residual: stage this layer's local Q (k-major) in
+    // shared memory; E_prev = S - P_o Q_loc^T is formed on the fly per row
+    const float* Ql = t.qloc + L.ql_off;
+    cta_sync1<NW * 32>();  // previous segment's readers are done
+    for (int idx = threadIdx.x; idx < RT * m4; idx += NW * 32) {
+      const int k = idx / m4, c = idx - k * m4;
+      *reinterpret_cast<float4*>(sh.sQl + k * m + 4 * c) = k < r ? ld_f4(Ql + k * m + 4 * c) : zero4();
+    }
+    cta_sync1<NW * 32>();
+  }
+  // x = M + S - sum_k po[k] Q_loc[k] (po = 0 when E is materialised)
+  auto corrected = [&](const float* tM, const float* tE, int toff, int i, const float (&po)[RT]) {
+    float4 xi = f4add(lds4(tM + toff + coff[i]), lds4(tE + toff + coff[i]));
+    if (defer) {
+#pragma unroll
+      for (int k = 0; k < RT; ++k) f4fma(xi, -po[k], lds4(sh.sQl + k * m + coff[i]));
+    }
+    return xi;
+  };
   for (int64_t r0 = s.row0; r0 < s.row1; r0 += TR) {
     const int nr = (int)((s.row1 - r0) < TR ? (s.row1 - r0) : TR);
     const int stage = pp.stage;
@@ -245,13 +266,16 @@ __device__ void seg_k1p(const Tables& t, const LayerDesc& L, const StreamSeg& s,
       // RT >= 8: x is re-read from shared memory for the residual (registers
       // go to the factor); the stage is then released after the residual
       constexpr bool kReload = RT >= 8;
+      float po[RT];
+#pragma unroll
+      for (int k = 0; k < RT; ++k) po[k] = (defer && k < r) ? Pw[(int64_t)k * n + r0 + (rval ? tri : 0)] : 0.f;
       float4 x[kReload ? 1 : NC];
       float acc[RT];
 #pragma unroll
       for (int k = 0; k < RT; ++k) acc[k] = 0.f;
 #pragma unroll
       for (int i = 0; i < NC; ++i) {
-        const float4 xi = f4add(lds4(tM + toff + coff[i]), lds4(tE + toff + coff[i]));
+        const float4 xi = corrected(tM, tE, toff, i, po);
         if constexpr (!kReload) x[i] = xi;
 #pragma unroll
         for (int k = 0; k < RT; ++k) {
@@ -296,7 +320,7 @@ __device__ void seg_k1p(const Tables& t, const LayerDesc& L, const StreamSeg& s,
 #pragma unroll
       for (int i = 0; i < NC; ++i) {
         float4 e;
-        if constexpr (kReload) e = f4add(lds4(tM + toff + coff[i]), lds4(tE + toff + coff[i]));
+        if constexpr (kReload) e = corrected(tM, tE, toff, i, po);
         else e = x[i];
 #pragma unroll
         for (int k = 0; k < RT; ++k) f4fma(e, -acc[k], qa[i][k]);
@@ -322,7 +346,7 @@ __device__ void seg_k1p(const Tables& t, const LayerDesc& L, const StreamSeg& s,
 template <int MODE, int RT, int NC>
 __device__ void seg_fast(const Tables& t, const LayerDesc& L, const StreamSeg& s,
                          float* __restrict__ grad, float scale, const Shared& sh, Pipe& pp,
-                         int& rph) {
+                         int& rph, int defer) {
   constexpr int NW = Cfg<MODE>::NW;
   const StreamMap mp = L.sm[ModeIdx<MODE>::v];
   const int lg = mp.lg, gw = mp.gw, rs = mp.rs, TR = mp.tr;
@@ -475,6 +499,12 @@ __device__ void seg_fast(const Tables& t, const LayerDesc& L, const StreamSeg& s
             }
           }
         } else {
+          if (defer) {  // deferred Q-step residual: keep S = M' in E
+            const int64_t rowg = r0 + tri;
+#pragma unroll
+            for (int i = 0; i < NC; ++i)
+              if (rval && cval[i]) st_cs4(E + rowg * m + coff[i], x[i]);
+          }
 #pragma unroll
           for (int i = 0; i < NC; ++i)
 #pragma unroll
@@ -541,7 +571,7 @@ __device__ __forceinline__ void block_sum(float (&a)[RT], float* red) {
 
 template <int MODE, int RT>
 __device__ void seg_generic(const Tables& t, const LayerDesc& L, const StreamSeg& s,
-                            float* __restrict__ grad, float scale, float* red) {
+                            float* __restrict__ grad, float scale, float* red, int defer) {
   constexpr int NT = Cfg<MODE>::NW * 32;
   const int64_t m = L.m, n = L.n;
   const int r = L.r;
@@ -564,6 +594,7 @@ __device__ void seg_generic(const Tables& t, const LayerDesc& L, const StreamSeg
         for (int k = 0; k < RT; ++k) acc[k] = 0.f;
         for (int64_t row = s.row0; row < s.row1; ++row) {
           const float x = grad[row * m + c] + E[row * m + c];
+          if (defer) E[row * m + c] = x;  // deferred residual: keep S = M'
 #pragma unroll
           for (int k = 0; k < RT; ++k)
             if (k < r) acc[k] = fmaf(x, __ldg(Ps + k * n + row), acc[k]);
@@ -579,11 +610,19 @@ __device__ void seg_generic(const Tables& t, const LayerDesc& L, const StreamSeg
     float* __restrict__ gr = grad + row * m;
     float* __restrict__ er = E + row * m;
     if constexpr (MODE == 0) {
+      float po[RT];  // deferred: E_prev = S - P_o Q_loc^T (P slot still holds P_o)
+#pragma unroll
+      for (int k = 0; k < RT; ++k) po[k] = (defer && k < r) ? Ps[k * n + row] : 0.f;
       float acc[RT];
 #pragma unroll
       for (int k = 0; k < RT; ++k) acc[k] = 0.f;
       for (int64_t j = threadIdx.x; j < m; j += NT) {
-        const float x = gr[j] + er[j];
+        float x = gr[j] + er[j];
+        if (defer) {
+#pragma unroll
+          for (int k = 0; k < RT; ++k)
+            if (k < r) x = fmaf(-po[k], __ldg(Ql + k * m + j), x);
+        }
 #pragma unroll
         for (int k = 0; k < RT; ++k)
           if (k < r) acc[k] = fmaf(x, __ldg(Qs + k * m + j), acc[k]);
@@ -591,11 +630,17 @@ __device__ void seg_generic(const Tables& t, const LayerDesc& L, const StreamSeg
       block_sum<NT, RT>(acc, red);
       for (int64_t j = threadIdx.x; j < m; j += NT) {
         float x = gr[j] + er[j];
+        if (defer) {
+#pragma unroll
+          for (int k = 0; k < RT; ++k)
+            if (k < r) x = fmaf(-po[k], __ldg(Ql + k * m + j), x);
+        }
 #pragma unroll
         for (int k = 0; k < RT; ++k)
           if (k < r) x = fmaf(-acc[k], __ldg(Qs + k * m + j), x);
         er[j] = x;
       }
+      cta_sync1<NT>();  // every thread has read P_o of this row before it is overwritten
       if (threadIdx.x == 0) {
 #pragma unroll
         for (int k = 0; k < RT; ++k)
@@ -624,7 +669,7 @@ __device__ void seg_generic(const Tables& t, const LayerDesc& L, const StreamSeg
 template <int MODE, int RT>
 __global__ void __launch_bounds__(Cfg<MODE>::NW * 32 + 32, Cfg<MODE>::CPS)
     stream_kernel(Tables t, const StreamSeg* __restrict__ segs, const int32_t* __restrict__ cta_begin,
-                  float scale, int stages, int stage_floats) {
+                  float scale, int stages, int stage_floats, int factor_floats, int defer) {
   constexpr int NT = Cfg<MODE>::NW * 32;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Shared sh;
@@ -637,7 +682,8 @@ __global__ void __launch_bounds__(Cfg<MODE>::NW * 32 + 32, Cfg<MODE>::CPS)
   sh.red = reinterpret_cast<float*>(sh.empty + stages);
   sh.gred = sh.red + 2 * 16 * 8;
   sh.cred = reinterpret_cast<float4*>(sh.gred + 16 * 32);
-  sh.flag = reinterpret_cast<int*>(sh.cred + 16 * 32);
+  sh.sQl = reinterpret_cast<float*>(sh.cred + 16 * 32);
+  sh.flag = reinterpret_cast<int*>(sh.sQl + factor_floats);
   if (threadIdx.x == 0) {
     for (int i = 0; i < stages; ++i) {
       mbar_init(&sh.full[i], 1);
@@ -647,6 +693,11 @@ __global__ void __launch_bounds__(Cfg<MODE>::NW * 32 + 32, Cfg<MODE>::CPS)
   }
   __syncthreads();
   const int sb = cta_begin[blockIdx.x], se = cta_begin[blockIdx.x + 1];
+  // deferred Q-step residual: K1 Q-step raises the flag (nothing in that
+  // launch reads it); K1 P-step reads it (cleared later by the P decode)
+  int dflag = 0;
+  if (MODE == 3 && defer && blockIdx.x == 0 && threadIdx.x == 0) *t.deferred = 1;
+  if (MODE == 0 && defer) dflag = *t.deferred;
   if ((threadIdx.x >> 5) == Cfg<MODE>::NW) {  // producer warp
     if ((threadIdx.x & 31) == 0) producer<MODE>(t, segs, sb, se, sh);
     return;
@@ -671,14 +722,14 @@ __global__ void __launch_bounds__(Cfg<MODE>::NW * 32 + 32, Cfg<MODE>::CPS)
       continue;
     }
     if (!is_fast<MODE>(L, grad)) {
-      seg_generic<MODE, RT>(t, L, s, grad, scale, sh.gred);
+      seg_generic<MODE, RT>(t, L, s, grad, scale, sh.gred, MODE == 0 ? dflag : defer);
     } else {
       switch (L.sm[ModeIdx<MODE>::v].nc) {
 #define ACP_CASE(NCV)                                                            \
   case NCV:                                                                      \
     if constexpr (NCV <= nc_max(MODE, RT)) {                                     \
-      if constexpr (MODE == 0) seg_k1p<RT, NCV>(t, L, s, sh, pp, rph);           \
-      else seg_fast<MODE, RT, NCV>(t, L, s, grad, scale, sh, pp, rph);          \
+      if constexpr (MODE == 0) seg_k1p<RT, NCV>(t, L, s, sh, pp, rph, dflag);    \
+      else seg_fast<MODE, RT, NCV>(t, L, s, grad, scale, sh, pp, rph, defer);   \
     }                                                                            \
     break;
         ACP_CASE(1)
@@ -695,12 +746,14 @@ __global__ void __launch_bounds__(Cfg<MODE>::NW * 32 + 32, Cfg<MODE>::CPS)
 
 template <int MODE>
 cudaError_t launch_mode(int rt, const Tables& t, const StreamSeg* segs, const int32_t* cb, int ncta,
-                        float scale, int stages, int stage_floats, cudaStream_t st) {
-  const size_t smem = stream_smem_bytes(stages, stage_floats);
+                        float scale, int stages, int stage_floats, int factor_floats, int defer,
+                        cudaStream_t st) {
+  const size_t smem = stream_smem_bytes(stages, stage_floats, factor_floats);
   auto go = [&](auto kern) -> cudaError_t {
     cudaError_t e = allow_max_smem(reinterpret_cast<const void*>(kern));
     if (e != cudaSuccess) return e;
-    kern<<<ncta, Cfg<MODE>::NW * 32 + 32, smem, st>>>(t, segs, cb, scale, stages, stage_floats);
+    kern<<<ncta, Cfg<MODE>::NW * 32 + 32, smem, st>>>(t, segs, cb, scale, stages, stage_floats,
+                                                      factor_floats, defer);
     return cudaGetLastError();
   };
   switch (rt) {
@@ -791,9 +844,9 @@ cudaError_t allow_max_smem(const void* kern) {
   return e;
 }
 
-size_t stream_smem_bytes(int stages, int stage_floats) {
+size_t stream_smem_bytes(int stages, int stage_floats, int factor_floats) {
   return (size_t)2 * stages * stage_floats * 4 + 2 * stages * 8 + (2 * 16 * 8 + 16 * 32) * 4 +
-         16 * 32 * 16 + 16;
+         16 * 32 * 16 + (size_t)factor_floats * 4 + 16;
 }
 
 // Host: choose the thread mapping of an m-column layer for stream mode
@@ -850,12 +903,12 @@ bool stream_make_map(int mode, int64_t m, int rt, StreamMap* out) {
 
 cudaError_t launch_stream(int mode, int rt, const Tables& t, const StreamSeg* segs,
                           const int32_t* cta_begin, int ncta, float scale, int stages,
-                          int stage_floats, cudaStream_t s) {
+                          int stage_floats, int factor_floats, int defer, cudaStream_t s) {
   if (ncta <= 0) return cudaSuccess;
   switch (mode) {
-    case 0: return launch_mode<0>(rt, t, segs, cta_begin, ncta, scale, stages, stage_floats, s);
-    case 2: return launch_mode<2>(rt, t, segs, cta_begin, ncta, scale, stages, stage_floats, s);
-    case 3: return launch_mode<3>(rt, t, segs, cta_begin, ncta, scale, stages, stage_floats, s);
+    case 0: return launch_mode<0>(rt, t, segs, cta_begin, ncta, scale, stages, stage_floats, factor_floats, defer, s);
+    case 2: return launch_mode<2>(rt, t, segs, cta_begin, ncta, scale, stages, stage_floats, factor_floats, defer, s);
+    case 3: return launch_mode<3>(rt, t, segs, cta_begin, ncta, scale, stages, stage_floats, factor_floats, defer, s);
     default: return cudaErrorInvalidValue;
   }
 }
