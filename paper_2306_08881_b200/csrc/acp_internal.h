@@ -152,13 +152,14 @@ cudaError_t allow_max_smem(const void* kern);
 // factor_floats of shared memory).
 cudaError_t launch_stream(int mode, int rt, const Tables& t, const StreamSeg* segs,
                           const int32_t* cta_begin, int ncta, float scale, int stages,
-                          int stage_floats, int factor_floats, int defer, cudaStream_t stream);
+                          int stage_floats, int factor_floats, int defer, int ptile,
+                          cudaStream_t stream);
 // E (or dst) = S - P Q_loc^T for one matrix layer (deferred state -> E)
 cudaError_t launch_materialize(const Tables& t, const LayerDesc& L, int layer, float* dst,
                                cudaStream_t stream);
 bool stream_make_map(int mode, int64_t m, int rt, StreamMap* out);
 int stream_ctas_per_sm(int mode);
-size_t stream_smem_bytes(int stages, int stage_floats, int factor_floats);
+size_t stream_smem_bytes(int stages, int stage_floats, int factor_floats, int ptile);
 // K2: CholeskyQR2 of the factors named by segs (side 0: Q factors in the
 // Q-buffer, length m; side 1: P factors in the P-buffer, length n).
 cudaError_t launch_orth(int rt, const Tables& t, int side, const OrthSeg* segs, int nseg,

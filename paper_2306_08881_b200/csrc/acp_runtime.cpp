@@ -41,7 +41,7 @@ struct Launch {
   int64_t seg_off = 0;   // first segment (row, col or stream array)
   int64_t cb_off = 0;    // first entry of cta_begin
   int ncta = 0;
-  int stages = 0, stage_floats = 0, factor_floats = 0, defer = 0;
+  int stages = 0, stage_floats = 0, factor_floats = 0, defer = 0, ptile = 0;
   int64_t red_off = 0;   // K1 Q-step: first ColReduceTask of this launch
   int nred = 0, nitems = 0;
   double bytes = 0;      // algorithmic bytes moved by this launch
@@ -348,11 +348,12 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
     return ln;
   };
   // TMA stream launch (mode 0: K1 P-step, 2: K3 Q-step, 3: K1 Q-step)
+  bool smem_overflow = false;
   auto stream_launch = [&](int mode, const std::vector<int>& tensors) {
     const int mi = mode == 0 ? 0 : (mode == 2 ? 1 : 2);
     std::vector<Unit> units;
     double bytes = 0;
-    int64_t stage_floats = 32, factor_floats = 0;
+    int64_t stage_floats = 32, factor_floats = 0, max_tr = 0;
     for (int i : tensors) {
       const LayerDesc& L = P.L[i];
       if (!L.mat) {
@@ -367,6 +368,7 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
       const int64_t pc = fast ? mp.pcols : L.m;
       const int np = fast ? mp.np : 1;
       if (fast) stage_floats = std::max<int64_t>(stage_floats, tr * pc);
+      if (fast) max_tr = std::max<int64_t>(max_tr, tr);
       if (fast && mode == 0 && P.defer)  // staged Q_loc [RT][m]
         factor_floats = std::max<int64_t>(factor_floats, (int64_t)P.RT * L.m);
       for (int pn = 0; pn < np; ++pn) {
@@ -385,11 +387,18 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
     ln.cb_off = (int64_t)P.ctab.size();
     stage_floats = (stage_floats + 31) / 32 * 32;
     const int cps = stream_ctas_per_sm(mode);
+    // P rows per stage (modes 2, 3 always; mode 0 when deferred): [tr][RT]
+    const bool need_p = mode != 0 || P.defer;
+    // row stride RT in sP; the kernel derives it as ptile / tr per layer, so
+    // size per-layer slots as tr_layer * RT and reserve max_tr * RT per stage
+    ln.ptile = need_p ? (int)(max_tr * P.RT) : 0;
     const int64_t budget = (cps == 1 ? 200 : 96) * 1024 - 4 * factor_floats;
-    int stages = (int)std::min<int64_t>(8, budget / (2 * 4 * stage_floats));
+    int stages = (int)std::min<int64_t>(8, budget / (2 * 4 * stage_floats + 4 * ln.ptile));
     ln.stages = std::max(2, stages);
     ln.stage_floats = (int)stage_floats;
     ln.factor_floats = (int)factor_floats;
+    if (stream_smem_bytes(ln.stages, ln.stage_floats, ln.factor_floats, ln.ptile) > 227 * 1024)
+      smem_overflow = true;
     ln.defer = (P.defer && (mode == 0 || mode == 3)) ? 1 : 0;
     int64_t part = 0;
     int prev_layer = -1, prev_panel = -1;
@@ -487,6 +496,7 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
     }
   }
   P.colcnt_n = std::max<int64_t>(P.colcnt_n, P.T);
+  if (smem_overflow) return fail(ACP_E_INVAL, "internal: stream kernel shared memory exceeds 227 KB");
   // K2 segments per side (0: Q factors, length m; 1: P factors, length n)
   for (int side = 0; side < 2; ++side) {
     int64_t g = 0;
@@ -644,7 +654,7 @@ acp_status run_k1(acp_ctx* c, int parity, const Launch& ln, cudaStream_t s) {
   cudaError_t e;
   if (ln.kind == 2) {
     e = launch_stream(ln.mode, c->P.RT, c->tab, dev_streamsegs(c, ln), dev_ctab(c, ln), ln.ncta,
-                      1.0f, ln.stages, ln.stage_floats, ln.factor_floats, ln.defer, s);
+                      1.0f, ln.stages, ln.stage_floats, ln.factor_floats, ln.defer, ln.ptile, s);
     if (e == cudaSuccess && ln.mode == 3 && ln.nred > 0) {
       e = launch_col_reduce(c->tab,
                             reinterpret_cast<const ColReduceTask*>(c->ws + c->P.off_red) + ln.red_off,
@@ -669,7 +679,8 @@ acp_status run_k3(acp_ctx* c, int parity, const Launch& ln, cudaStream_t s) {
   cudaError_t e =
       ln.kind == 2
           ? launch_stream(ln.mode, c->P.RT, c->tab, dev_streamsegs(c, ln), dev_ctab(c, ln), ln.ncta,
-                          decode_scale(c), ln.stages, ln.stage_floats, ln.factor_floats, ln.defer, s)
+                          decode_scale(c), ln.stages, ln.stage_floats, ln.factor_floats, ln.defer,
+                          ln.ptile, s)
           : launch_row(ln.mode, c->P.RT, c->tab, dev_rowsegs(c, ln), dev_ctab(c, ln),
                        ln.ncta, decode_scale(c), ef, s);
   prof_end(r, s);

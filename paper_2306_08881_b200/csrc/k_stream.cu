@@ -117,6 +117,8 @@ struct Shared {
   float* gred;   // generic path block reduction [16][32]
   float4* cred;  // column mode: cross-row-slot combine [NW*32]
   float* sQl;    // K1-P deferred: local Q factor of the segment's layer [RT][m]
+  float* sP;     // per stage: the tile's P rows [tr][RT] (staged by the producer warp)
+  int ptile;     // floats per stage in sP
   int* flag;
   int stage_floats;
   int stages;
@@ -145,7 +147,12 @@ __device__ __forceinline__ bool is_fast(const LayerDesc& L, const float* grad) {
 // Producer warp (lane 0): walk the CTA's segments and issue every bulk tile
 // as soon as its ring stage is released by all consumer warps.
 template <int MODE>
-__device__ void producer(const Tables& t, const StreamSeg* segs, int sb, int se, const Shared& sh) {
+__device__ void producer(const Tables& t, const StreamSeg* segs, int sb, int se, const Shared& sh,
+                         int stage_p) {
+  // lane 0 drives the ring (waits + bulk copies); when the consumers need the
+  // tile's rows of the P factor (stage_p), the whole warp gathers them into
+  // the stage's sP slot ([row][RT], zero-padded) before lane 0 arms the stage
+  const int lane = threadIdx.x & 31;
   const uint64_t pol = policy_evict_first();
   int stage = 0;
   uint32_t phase = 0;
@@ -155,28 +162,42 @@ __device__ void producer(const Tables& t, const StreamSeg* segs, int sb, int se,
     const float* grad = t.grads[s.layer];
     if (!is_fast<MODE>(L, grad)) continue;
     const StreamMap mp = L.sm[ModeIdx<MODE>::v];
-    const int64_t m = L.m;
+    const int64_t m = L.m, n = L.n;
+    const int r = L.r;
     const int tr = mp.tr;
     const int64_t c0 = (int64_t)s.panel * mp.pcols;
     const int64_t cols = (m - c0) < mp.pcols ? (m - c0) : mp.pcols;
     const float* pm = grad + s.row0 * m + c0;
     const float* pe = t.E + L.e_off + s.row0 * m + c0;
+    const float* Pf = t.pbuf + L.p_off;
+    const int RTp = sh.ptile > 0 ? sh.ptile / tr : 0;  // row stride in sP (>= r)
     for (int64_t r0 = s.row0; r0 < s.row1; r0 += tr) {
       const int64_t nr = (s.row1 - r0) < tr ? (s.row1 - r0) : tr;
-      mbar_wait(&sh.empty[stage], phase ^ 1u);
-      float* dM = sh.sM + (size_t)stage * sh.stage_floats;
-      float* dE = sh.sE + (size_t)stage * sh.stage_floats;
-      if (cols == m) {  // whole rows: one contiguous copy per tensor
-        const uint32_t bytes = (uint32_t)(nr * m * 4);
-        mbar_arrive_tx(&sh.full[stage], 2 * bytes);
-        bulk_g2s(dM, pm, bytes, &sh.full[stage], pol);
-        bulk_g2s(dE, pe, bytes, &sh.full[stage], pol);
-      } else {          // panel: one copy per row, smem row stride pcols
-        const uint32_t rb = (uint32_t)(cols * 4);
-        mbar_arrive_tx(&sh.full[stage], (uint32_t)(2 * nr) * rb);
-        for (int64_t i = 0; i < nr; ++i) {
-          bulk_g2s(dM + i * mp.pcols, pm + i * m, rb, &sh.full[stage], pol);
-          bulk_g2s(dE + i * mp.pcols, pe + i * m, rb, &sh.full[stage], pol);
+      if (lane == 0) mbar_wait(&sh.empty[stage], phase ^ 1u);
+      __syncwarp();
+      if (stage_p && sh.ptile > 0) {
+        float* dP = sh.sP + (size_t)stage * sh.ptile;
+        for (int idx = lane; idx < tr * RTp; idx += 32) {
+          const int i = idx / RTp, k = idx - i * RTp;
+          dP[idx] = (i < nr && k < r) ? Pf[(int64_t)k * n + r0 + i] : 0.f;
+        }
+        __syncwarp();
+      }
+      if (lane == 0) {
+        float* dM = sh.sM + (size_t)stage * sh.stage_floats;
+        float* dE = sh.sE + (size_t)stage * sh.stage_floats;
+        if (cols == m) {  // whole rows: one contiguous copy per tensor
+          const uint32_t bytes = (uint32_t)(nr * m * 4);
+          mbar_arrive_tx(&sh.full[stage], 2 * bytes);
+          bulk_g2s(dM, pm, bytes, &sh.full[stage], pol);
+          bulk_g2s(dE, pe, bytes, &sh.full[stage], pol);
+        } else {          // panel: one copy per row, smem row stride pcols
+          const uint32_t rb = (uint32_t)(cols * 4);
+          mbar_arrive_tx(&sh.full[stage], (uint32_t)(2 * nr) * rb);
+          for (int64_t i = 0; i < nr; ++i) {
+            bulk_g2s(dM + i * mp.pcols, pm + i * m, rb, &sh.full[stage], pol);
+            bulk_g2s(dE + i * mp.pcols, pe + i * m, rb, &sh.full[stage], pol);
+          }
         }
       }
       pm += nr * m;
@@ -266,9 +287,12 @@ __device__ void seg_k1p(const Tables& t, const LayerDesc& L, const StreamSeg& s,
       // RT >= 8: x is re-read from shared memory for the residual (registers
       // go to the factor); the stage is then released after the residual
       constexpr bool kReload = RT >= 8;
-      float po[RT];
+      float po[RT];  // P_o row staged by the producer (zero beyond r)
+      {
+        const float* ps = sh.sP + (size_t)stage * sh.ptile + (rval ? tri : 0) * (sh.ptile / TR);
 #pragma unroll
-      for (int k = 0; k < RT; ++k) po[k] = (defer && k < r) ? Pw[(int64_t)k * n + r0 + (rval ? tri : 0)] : 0.f;
+        for (int k = 0; k < RT; ++k) po[k] = defer ? ps[k] : 0.f;
+      }
       float4 x[kReload ? 1 : NC];
       float acc[RT];
 #pragma unroll
@@ -481,9 +505,12 @@ __device__ void seg_fast(const Tables& t, const LayerDesc& L, const StreamSeg& s
             if (k < r) t.pbuf[L.p_off + (int64_t)k * n + row] = acc[k];
         }
       } else {
-        float pk[RT];
+        float pk[RT];  // P row staged by the producer (zero beyond r)
+        {
+          const float* ps = sh.sP + (size_t)stage * sh.ptile + (rval ? tri : 0) * (sh.ptile / TR);
 #pragma unroll
-        for (int k = 0; k < RT; ++k) pk[k] = (k < r) ? __ldg(Pf + (int64_t)k * n + row) : 0.f;
+          for (int k = 0; k < RT; ++k) pk[k] = ps[k];
+        }
         if constexpr (MODE == 2) {
 #pragma unroll
           for (int i = 0; i < NC; ++i) {
@@ -669,7 +696,8 @@ __device__ void seg_generic(const Tables& t, const LayerDesc& L, const StreamSeg
 template <int MODE, int RT>
 __global__ void __launch_bounds__(Cfg<MODE>::NW * 32 + 32, Cfg<MODE>::CPS)
     stream_kernel(Tables t, const StreamSeg* __restrict__ segs, const int32_t* __restrict__ cta_begin,
-                  float scale, int stages, int stage_floats, int factor_floats, int defer) {
+                  float scale, int stages, int stage_floats, int factor_floats, int defer,
+                  int ptile) {
   constexpr int NT = Cfg<MODE>::NW * 32;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Shared sh;
@@ -683,7 +711,9 @@ __global__ void __launch_bounds__(Cfg<MODE>::NW * 32 + 32, Cfg<MODE>::CPS)
   sh.gred = sh.red + 2 * 16 * 8;
   sh.cred = reinterpret_cast<float4*>(sh.gred + 16 * 32);
   sh.sQl = reinterpret_cast<float*>(sh.cred + 16 * 32);
-  sh.flag = reinterpret_cast<int*>(sh.sQl + factor_floats);
+  sh.sP = sh.sQl + factor_floats;
+  sh.ptile = ptile;
+  sh.flag = reinterpret_cast<int*>(sh.sP + (size_t)stages * ptile);
   if (threadIdx.x == 0) {
     for (int i = 0; i < stages; ++i) {
       mbar_init(&sh.full[i], 1);
@@ -699,7 +729,7 @@ __global__ void __launch_bounds__(Cfg<MODE>::NW * 32 + 32, Cfg<MODE>::CPS)
   if (MODE == 3 && defer && blockIdx.x == 0 && threadIdx.x == 0) *t.deferred = 1;
   if (MODE == 0 && defer) dflag = *t.deferred;
   if ((threadIdx.x >> 5) == Cfg<MODE>::NW) {  // producer warp
-    if ((threadIdx.x & 31) == 0) producer<MODE>(t, segs, sb, se, sh);
+    producer<MODE>(t, segs, sb, se, sh, MODE == 0 ? dflag : 1);
     return;
   }
   Pipe pp;
@@ -747,13 +777,13 @@ __global__ void __launch_bounds__(Cfg<MODE>::NW * 32 + 32, Cfg<MODE>::CPS)
 template <int MODE>
 cudaError_t launch_mode(int rt, const Tables& t, const StreamSeg* segs, const int32_t* cb, int ncta,
                         float scale, int stages, int stage_floats, int factor_floats, int defer,
-                        cudaStream_t st) {
-  const size_t smem = stream_smem_bytes(stages, stage_floats, factor_floats);
+                        int ptile, cudaStream_t st) {
+  const size_t smem = stream_smem_bytes(stages, stage_floats, factor_floats, ptile);
   auto go = [&](auto kern) -> cudaError_t {
     cudaError_t e = allow_max_smem(reinterpret_cast<const void*>(kern));
     if (e != cudaSuccess) return e;
     kern<<<ncta, Cfg<MODE>::NW * 32 + 32, smem, st>>>(t, segs, cb, scale, stages, stage_floats,
-                                                      factor_floats, defer);
+                                                      factor_floats, defer, ptile);
     return cudaGetLastError();
   };
   switch (rt) {
@@ -844,9 +874,9 @@ cudaError_t allow_max_smem(const void* kern) {
   return e;
 }
 
-size_t stream_smem_bytes(int stages, int stage_floats, int factor_floats) {
+size_t stream_smem_bytes(int stages, int stage_floats, int factor_floats, int ptile) {
   return (size_t)2 * stages * stage_floats * 4 + 2 * stages * 8 + (2 * 16 * 8 + 16 * 32) * 4 +
-         16 * 32 * 16 + (size_t)factor_floats * 4 + 16;
+         16 * 32 * 16 + (size_t)factor_floats * 4 + (size_t)stages * ptile * 4 + 16;
 }
 
 // Host: choose the thread mapping of an m-column layer for stream mode
@@ -876,7 +906,8 @@ bool stream_make_map(int mode, int64_t m, int rt, StreamMap* out) {
     int lg = 1;
     while (lg < pc4) lg <<= 1;
     const int64_t nrs = (int64_t)NW * (32 / lg);
-    const int64_t rs = std::max<int64_t>(1, TT / (nrs * pcols));
+    // tiles of at most TT floats and 256 rows (the staged P rows grow with tr)
+    const int64_t rs = std::max<int64_t>(1, std::min<int64_t>(TT / (nrs * pcols), 256 / nrs));
     out->lg = (int16_t)lg;
     out->gw = 1;
     out->nc = 1;
@@ -903,12 +934,12 @@ bool stream_make_map(int mode, int64_t m, int rt, StreamMap* out) {
 
 cudaError_t launch_stream(int mode, int rt, const Tables& t, const StreamSeg* segs,
                           const int32_t* cta_begin, int ncta, float scale, int stages,
-                          int stage_floats, int factor_floats, int defer, cudaStream_t s) {
+                          int stage_floats, int factor_floats, int defer, int ptile, cudaStream_t s) {
   if (ncta <= 0) return cudaSuccess;
   switch (mode) {
-    case 0: return launch_mode<0>(rt, t, segs, cta_begin, ncta, scale, stages, stage_floats, factor_floats, defer, s);
-    case 2: return launch_mode<2>(rt, t, segs, cta_begin, ncta, scale, stages, stage_floats, factor_floats, defer, s);
-    case 3: return launch_mode<3>(rt, t, segs, cta_begin, ncta, scale, stages, stage_floats, factor_floats, defer, s);
+    case 0: return launch_mode<0>(rt, t, segs, cta_begin, ncta, scale, stages, stage_floats, factor_floats, defer, ptile, s);
+    case 2: return launch_mode<2>(rt, t, segs, cta_begin, ncta, scale, stages, stage_floats, factor_floats, defer, ptile, s);
+    case 3: return launch_mode<3>(rt, t, segs, cta_begin, ncta, scale, stages, stage_floats, factor_floats, defer, ptile, s);
     default: return cudaErrorInvalidValue;
   }
 }
