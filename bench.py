@@ -180,6 +180,19 @@ def run_reference(args):
     return 0
 
 
+def max_over_ranks(value: float) -> float:
+    """Max of a per-rank scalar over the default process group (the bench's
+    timing rule: a multi-GPU step takes as long as its slowest rank)."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(value)
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([float(value)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def _setup_dist(args):
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -229,11 +242,7 @@ def _measure(model, r, world, rank, local, args, comm, profile=True):
         if world > 1:
             torch.distributed.barrier()
     launches = ctx.launch_count() - l0
-    ms = ev0.elapsed_time(ev1) / args.steps
-    if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
     prof = None
     if profile:
         # per-kernel CUDA events on the launching stream (eager launches)
@@ -276,11 +285,7 @@ def _e2e(res, world, args):
         one(t + 1)
     ev1.record(stream)
     torch.cuda.synchronize()
-    ms = ev0.elapsed_time(ev1) / steps
-    if world > 1:
-        tt = torch.tensor([ms], device="cuda")
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        ms = float(tt.item())
+    ms = max_over_ranks(ev0.elapsed_time(ev1) / steps)
     nbytes = 4 * res["nel"]
     return {"value": world * nbytes / (ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": ms,
             "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "steps": steps}

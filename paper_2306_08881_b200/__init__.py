@@ -6,6 +6,7 @@ loads the library and fails loudly if it has not been built.
 """
 from ._lib import (load as _load, AcpError, ACP_NO_EF, ACP_NO_REUSE, ACP_SUM,  # noqa: F401
                    LIB_PATH, EXPORTED)
-from .acp import AcpContext, nccl_comm_from_group, nccl_comm_destroy, DEFAULT_BUCKET_BYTES  # noqa: F401
+from .acp import (AcpContext, nccl_comm_from_group, nccl_comm_destroy, broadcast_unique_id,  # noqa: F401
+                  DEFAULT_BUCKET_BYTES)
 
 _load()

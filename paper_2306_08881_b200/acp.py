@@ -36,6 +36,18 @@ def _stream_handle(stream) -> int:
     return int(stream.cuda_stream)
 
 
+def broadcast_unique_id(uid: bytes, group=None) -> bytes:
+    """Broadcast group-rank 0's 128-byte NCCL unique id over ``group`` (any
+    torch.distributed backend); every rank returns rank 0's bytes."""
+    import torch.distributed as dist
+    if len(uid) != 128:
+        raise ValueError("an ncclUniqueId is 128 bytes")
+    payload = [bytes(uid)]
+    src = dist.get_global_rank(group, 0) if group is not None else 0
+    dist.broadcast_object_list(payload, src=src, group=group)
+    return payload[0]
+
+
 def nccl_comm_from_group(group=None, device: Optional[int] = None) -> int:
     """Create an NCCL communicator spanning ``group`` (torch.distributed):
     rank 0 draws the unique id, the group broadcasts it, every rank inits."""
@@ -46,10 +58,7 @@ def nccl_comm_from_group(group=None, device: Optional[int] = None) -> int:
     uid = (C.c_uint8 * 128)()
     if rank == 0:
         L.check(lib.acp_nccl_unique_id(uid))
-    payload = [bytes(uid)]
-    dist.broadcast_object_list(payload, src=dist.get_global_rank(group, 0) if group else 0,
-                               group=group)
-    uid = (C.c_uint8 * 128).from_buffer_copy(payload[0])
+    uid = (C.c_uint8 * 128).from_buffer_copy(broadcast_unique_id(bytes(uid), group))
     dev = torch.cuda.current_device() if device is None else device
     comm = C.c_void_p()
     L.check(lib.acp_nccl_comm_create(uid, world, rank, dev, C.byref(comm)))

@@ -27,3 +27,12 @@ def cuda_available():
         return torch.cuda.is_available()
     except Exception:
         return False
+
+
+def ensure_built():
+    """Build lib/libacp.so with nvcc if it is missing (no GPU needed)."""
+    lib = os.path.join(ROOT, "paper_2306_08881_b200", "lib", "libacp.so")
+    if not os.path.exists(lib):
+        from paper_2306_08881_b200 import build as B
+        B.build()
+    return lib

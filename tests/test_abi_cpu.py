@@ -8,7 +8,7 @@ import subprocess
 
 import pytest
 
-from conftest import ROOT
+from conftest import ROOT, ensure_built
 
 HEADER = os.path.join(ROOT, "include", "acp.h")
 
@@ -19,9 +19,7 @@ def _lib_path():
 
 @pytest.fixture(scope="module")
 def lib():
-    if not os.path.exists(_lib_path()):
-        from paper_2306_08881_b200 import build as B  # builds with nvcc (no GPU needed)
-        B.build()
+    ensure_built()  # nvcc cross-compiles; no GPU needed
     from paper_2306_08881_b200 import _lib
     return _lib.load()
 
