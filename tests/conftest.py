@@ -33,6 +33,15 @@ def ensure_built():
     """Build lib/libacp.so with nvcc if it is missing (no GPU needed)."""
     lib = os.path.join(ROOT, "paper_2306_08881_b200", "lib", "libacp.so")
     if not os.path.exists(lib):
-        from paper_2306_08881_b200 import build as B
-        B.build()
+        _load_build_module().build()
     return lib
+
+
+def _load_build_module():
+    # loaded by path: importing the package itself requires the built library
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "acp_build", os.path.join(ROOT, "paper_2306_08881_b200", "build.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
