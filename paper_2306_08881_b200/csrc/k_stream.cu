@@ -98,6 +98,16 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(s32(bar)), "l"(policy)
       : "memory");
 }
+// 4-byte async copy global -> shared (LDGSTS); src_bytes = 0 zero-fills
+__device__ __forceinline__ void cp_async4(float* dst, const float* src, uint32_t src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(s32(dst)), "l"(src),
+               "r"(src_bytes)
+               : "memory");
+}
+// arrive on `bar` once all of this thread's prior cp.async have landed
+__device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared.b64 [%0];" ::"r"(s32(bar)) : "memory");
+}
 template <int NT>
 __device__ __forceinline__ void cta_sync1() {
   asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
@@ -175,14 +185,6 @@ __device__ void producer(const Tables& t, const StreamSeg* segs, int sb, int se,
       const int64_t nr = (s.row1 - r0) < tr ? (s.row1 - r0) : tr;
       if (lane == 0) mbar_wait(&sh.empty[stage], phase ^ 1u);
       __syncwarp();
-      if (stage_p && sh.ptile > 0) {
-        float* dP = sh.sP + (size_t)stage * sh.ptile;
-        for (int idx = lane; idx < tr * RTp; idx += 32) {
-          const int i = idx / RTp, k = idx - i * RTp;
-          dP[idx] = (i < nr && k < r) ? Pf[(int64_t)k * n + r0 + i] : 0.f;
-        }
-        __syncwarp();
-      }
       if (lane == 0) {
         float* dM = sh.sM + (size_t)stage * sh.stage_floats;
         float* dE = sh.sE + (size_t)stage * sh.stage_floats;
@@ -199,6 +201,18 @@ __device__ void producer(const Tables& t, const StreamSeg* segs, int sb, int se,
             bulk_g2s(dE + i * mp.pcols, pe + i * m, rb, &sh.full[stage], pol);
           }
         }
+      }
+      if (stage_p) {
+        // the tile's P rows, gathered with async 4-byte copies (zero-filled
+        // beyond r / nr); each lane's arrive fires when its copies landed, so
+        // the producer never waits on these loads
+        float* dP = sh.sP + (size_t)stage * sh.ptile;
+        for (int idx = lane; idx < tr * RTp; idx += 32) {
+          const int i = idx / RTp, k = idx - i * RTp;
+          const bool ok = i < nr && k < r;
+          cp_async4(dP + idx, ok ? Pf + (int64_t)k * n + r0 + i : Pf, ok ? 4u : 0u);
+        }
+        cp_async_arrive(&sh.full[stage]);
       }
       pm += nr * m;
       pe += nr * m;
@@ -714,9 +728,12 @@ __global__ void __launch_bounds__(Cfg<MODE>::NW * 32 + 32, Cfg<MODE>::CPS)
   sh.sP = sh.sQl + factor_floats;
   sh.ptile = ptile;
   sh.flag = reinterpret_cast<int*>(sh.sP + (size_t)stages * ptile);
+  // the producer warp stages P rows (32 cp.async arrivals per tile) for the
+  // Q-step kernels and, when the residual is deferred, for the P-step one
+  const int stage_p = (ptile > 0) && (MODE != 0 || (defer && *t.deferred));
   if (threadIdx.x == 0) {
     for (int i = 0; i < stages; ++i) {
-      mbar_init(&sh.full[i], 1);
+      mbar_init(&sh.full[i], stage_p ? 33 : 1);
       mbar_init(&sh.empty[i], Cfg<MODE>::NW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -729,7 +746,7 @@ __global__ void __launch_bounds__(Cfg<MODE>::NW * 32 + 32, Cfg<MODE>::CPS)
   if (MODE == 3 && defer && blockIdx.x == 0 && threadIdx.x == 0) *t.deferred = 1;
   if (MODE == 0 && defer) dflag = *t.deferred;
   if ((threadIdx.x >> 5) == Cfg<MODE>::NW) {  // producer warp
-    producer<MODE>(t, segs, sb, se, sh, MODE == 0 ? dflag : 1);
+    producer<MODE>(t, segs, sb, se, sh, stage_p);
     return;
   }
   Pipe pp;
