@@ -302,28 +302,35 @@ __device__ __forceinline__ void block_sum(float (&a)[RT], float* red) {
 template <int MODE, int RT>
 __device__ void row_generic(const Tables& t, const LayerDesc& L, float* __restrict__ grad,
                             int64_t row0, int64_t row1, float scale, int ef, float* red) {
+  // one warp per row (lanes stride the columns, shuffle row sums): layers with
+  // many short rows (or m % 4 != 0) run without CTA barriers
+  (void)red;
   const int64_t m = L.m, n = L.n;
   const int r = L.r;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const float* __restrict__ Qs = t.qbuf + L.q_off;
   const float* __restrict__ Ql = t.qloc + L.ql_off;
   float* __restrict__ Ps = t.pbuf + L.p_off;
   float* __restrict__ E = t.E + L.e_off;
-  for (int64_t row = row0; row < row1; ++row) {
+  for (int64_t row = row0 + warp; row < row1; row += kThreads / 32) {
     float* __restrict__ g = grad + row * m;
     float* __restrict__ e = E + row * m;
     if (MODE == 0) {
       float acc[RT];
 #pragma unroll
       for (int k = 0; k < RT; ++k) acc[k] = 0.f;
-      for (int64_t j = threadIdx.x; j < m; j += kThreads) {
+      for (int64_t j = lane; j < m; j += 32) {
         const float x = g[j] + (ef ? e[j] : 0.f);
 #pragma unroll
         for (int k = 0; k < RT; ++k)
           if (k < r) acc[k] = fmaf(x, __ldg(Qs + k * m + j), acc[k]);
       }
-      block_sum<RT>(acc, red);
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+        for (int k = 0; k < RT; ++k) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], off);
       if (ef) {
-        for (int64_t j = threadIdx.x; j < m; j += kThreads) {
+        for (int64_t j = lane; j < m; j += 32) {
           float x = g[j] + e[j];
 #pragma unroll
           for (int k = 0; k < RT; ++k)
@@ -331,7 +338,7 @@ __device__ void row_generic(const Tables& t, const LayerDesc& L, float* __restri
           e[j] = x;
         }
       }
-      if (threadIdx.x == 0) {
+      if (lane == 0) {
 #pragma unroll
         for (int k = 0; k < RT; ++k)
           if (k < r) Ps[k * n + row] = acc[k];
@@ -340,7 +347,7 @@ __device__ void row_generic(const Tables& t, const LayerDesc& L, float* __restri
       float p[RT];
 #pragma unroll
       for (int k = 0; k < RT; ++k) p[k] = (k < r) ? __ldg(Ps + k * n + row) : 0.f;
-      for (int64_t j = threadIdx.x; j < m; j += kThreads) {
+      for (int64_t j = lane; j < m; j += 32) {
         float o = 0.f;
         if (MODE == 1) {
 #pragma unroll

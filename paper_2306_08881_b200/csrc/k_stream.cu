@@ -613,9 +613,17 @@ __device__ __forceinline__ void block_sum(float (&a)[RT], float* red) {
 template <int MODE, int RT>
 __device__ void seg_generic(const Tables& t, const LayerDesc& L, const StreamSeg& s,
                             float* __restrict__ grad, float scale, float* red, int defer) {
-  constexpr int NT = Cfg<MODE>::NW * 32;
+  // Generic path (m % 4 != 0, very wide m, or an unaligned gradient): plain
+  // coalesced scalar accesses. Rows are spread over the warps (one warp per
+  // row, lanes stride the columns, warp-shuffle row sums) so a layer with many
+  // short rows does not serialise on CTA barriers; the column reduction
+  // (mode 3) gives each thread a column and unrolls its row loop.
+  constexpr int NWc = Cfg<MODE>::NW;
+  constexpr int NT = NWc * 32;
+  (void)red;
   const int64_t m = L.m, n = L.n;
   const int r = L.r;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const float* __restrict__ Qs = t.qbuf + L.q_off;
   const float* __restrict__ Ql = t.qloc + L.ql_off;
   float* __restrict__ Ps = t.pbuf + L.p_off;
@@ -633,9 +641,22 @@ __device__ void seg_generic(const Tables& t, const LayerDesc& L, const StreamSeg
         float acc[RT];
 #pragma unroll
         for (int k = 0; k < RT; ++k) acc[k] = 0.f;
-        for (int64_t row = s.row0; row < s.row1; ++row) {
+        int64_t row = s.row0;
+        for (; row + 4 <= s.row1; row += 4) {
+          float x[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) x[u] = grad[(row + u) * m + c] + E[(row + u) * m + c];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (defer) E[(row + u) * m + c] = x[u];  // deferred residual: keep S = M'
+#pragma unroll
+            for (int k = 0; k < RT; ++k)
+              if (k < r) acc[k] = fmaf(x[u], __ldg(Ps + k * n + row + u), acc[k]);
+          }
+        }
+        for (; row < s.row1; ++row) {
           const float x = grad[row * m + c] + E[row * m + c];
-          if (defer) E[row * m + c] = x;  // deferred residual: keep S = M'
+          if (defer) E[row * m + c] = x;
 #pragma unroll
           for (int k = 0; k < RT; ++k)
             if (k < r) acc[k] = fmaf(x, __ldg(Ps + k * n + row), acc[k]);
@@ -647,7 +668,7 @@ __device__ void seg_generic(const Tables& t, const LayerDesc& L, const StreamSeg
     }
     return;
   }
-  for (int64_t row = s.row0; row < s.row1; ++row) {
+  for (int64_t row = s.row0 + warp; row < s.row1; row += NWc) {
     float* __restrict__ gr = grad + row * m;
     float* __restrict__ er = E + row * m;
     if constexpr (MODE == 0) {
@@ -657,7 +678,7 @@ __device__ void seg_generic(const Tables& t, const LayerDesc& L, const StreamSeg
       float acc[RT];
 #pragma unroll
       for (int k = 0; k < RT; ++k) acc[k] = 0.f;
-      for (int64_t j = threadIdx.x; j < m; j += NT) {
+      for (int64_t j = lane; j < m; j += 32) {
         float x = gr[j] + er[j];
         if (defer) {
 #pragma unroll
@@ -668,8 +689,11 @@ __device__ void seg_generic(const Tables& t, const LayerDesc& L, const StreamSeg
         for (int k = 0; k < RT; ++k)
           if (k < r) acc[k] = fmaf(x, __ldg(Qs + k * m + j), acc[k]);
       }
-      block_sum<NT, RT>(acc, red);
-      for (int64_t j = threadIdx.x; j < m; j += NT) {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+        for (int k = 0; k < RT; ++k) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], off);
+      for (int64_t j = lane; j < m; j += 32) {
         float x = gr[j] + er[j];
         if (defer) {
 #pragma unroll
@@ -681,8 +705,8 @@ __device__ void seg_generic(const Tables& t, const LayerDesc& L, const StreamSeg
           if (k < r) x = fmaf(-acc[k], __ldg(Qs + k * m + j), x);
         er[j] = x;
       }
-      cta_sync1<NT>();  // every thread has read P_o of this row before it is overwritten
-      if (threadIdx.x == 0) {
+      __syncwarp();  // every lane has read P_o of this row
+      if (lane == 0) {
 #pragma unroll
         for (int k = 0; k < RT; ++k)
           if (k < r) Ps[k * n + row] = acc[k];
@@ -691,7 +715,7 @@ __device__ void seg_generic(const Tables& t, const LayerDesc& L, const StreamSeg
       float p[RT];
 #pragma unroll
       for (int k = 0; k < RT; ++k) p[k] = (k < r) ? __ldg(Ps + k * n + row) : 0.f;
-      for (int64_t j = c0 + threadIdx.x; j < c1; j += NT) {
+      for (int64_t j = c0 + lane; j < c1; j += 32) {
         float x = gr[j] + er[j], o = 0.f;
 #pragma unroll
         for (int k = 0; k < RT; ++k) {
