@@ -347,7 +347,11 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
     ln.bytes = bytes;
     return ln;
   };
-  // TMA stream launch (mode 0: K1 P-step, 2: K3 Q-step, 3: K1 Q-step)
+  // TMA stream launch (mode 0: K1 P-step, 2: K3 Q-step, 3: K1 Q-step).
+  // stream_waves > 1 over-decomposes the grid so the hardware CTA scheduler
+  // balances layers whose per-byte cost differs (dynamic load balance).
+  int stream_waves = 1;
+  if (const char* env = std::getenv("ACP_STREAM_WAVES")) stream_waves = std::max(1, std::atoi(env));
   bool smem_overflow = false;
   auto stream_launch = [&](int mode, const std::vector<int>& tensors) {
     const int mi = mode == 0 ? 0 : (mode == 2 ? 1 : 2);
@@ -403,7 +407,7 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
     int64_t part = 0;
     int prev_layer = -1, prev_panel = -1;
     ln.red_off = (int64_t)P.redtasks.size();
-    ln.ncta = split_units(units, min_share, nsm * cps, P.ctab, [&](const Unit& u, int64_t a, int64_t b) {
+    ln.ncta = split_units(units, min_share, nsm * cps * stream_waves, P.ctab, [&](const Unit& u, int64_t a, int64_t b) {
       StreamSeg s{};
       s.layer = u.layer;
       s.row0 = a;
