@@ -206,7 +206,7 @@ def _setup_dist(args):
     return world, rank, local
 
 
-def _measure(model, r, world, rank, local, args, comm, profile=True):
+def _measure(model, r, world, rank, local, args, comm, profile=True, flags=0):
     """Time K steps (CUDA-graph replay, the library default), then K more
     steps run eagerly with per-kernel CUDA events for the roofline."""
     import torch
@@ -220,7 +220,7 @@ def _measure(model, r, world, rank, local, args, comm, profile=True):
         g = torch.rand(s, device="cuda", generator=gen) * 2 - 1
         grads.append((g / (m ** 0.5)).contiguous())
     ctx = AcpContext(shapes, r, world_size=world, nccl_comm=comm, seed=7,
-                     bucket_bytes=args.bucket_bytes)
+                     bucket_bytes=args.bucket_bytes, flags=flags)
     ctx.set_graphs(not args.no_graphs)
     stream = torch.cuda.current_stream()
     for t in range(args.warmup):
@@ -343,6 +343,18 @@ def run_ours(args):
                      "roofline": _roofline(s["prof"], peak, peak_kind, args.secondary),
                      "gpu_launches": s["launches"]}
         s["ctx"].close()
+    psgd = None
+    if not args.no_powersgd and r <= 8:
+        # NEXT-1 / NEXT-4 context: the Power-SGD baseline (two projections and
+        # two all-reduces per step) through the same library
+        from paper_2306_08881_b200 import ACP_POWERSGD
+        torch.cuda.empty_cache()
+        ps = _measure(model, r, world, rank, local, args, comm, profile=False, flags=ACP_POWERSGD)
+        psgd = {"workload": args.workload, "ms_per_step": ps["ms"],
+                "value": world * 4.0 * ps["nel"] / (ps["ms"] * 1e-3) / 1e9, "unit": "GB/s",
+                "acp_speedup": ps["ms"] / ms, "gpu_launches": ps["launches"]}
+        ps["ctx"].close()
+        del ps
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = time_oracle(model, r, 2, 1, frac_every=args.oracle_every)
@@ -368,6 +380,7 @@ def run_ours(args):
             "clocks": res["clocks"],
             "gpu_launches": res["launches"],
             "secondary": secondary,
+            "powersgd": psgd,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -389,6 +402,8 @@ def main(argv=None):
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graphs", action="store_true")
+    ap.add_argument("--no-powersgd", action="store_true",
+                    help="skip the on-box Power-SGD comparison line")
     ap.add_argument("--oracle-every", type=int, default=3)
     args = ap.parse_args(argv)
     if args.warmup < 3:

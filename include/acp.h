@@ -83,7 +83,16 @@ enum {
   ACP_NO_REUSE = 2u,  /* query reuse off: orthogonalise a fresh seeded N(0,1)
                          factor each step instead of the previous aggregated
                          one (ablation, C12)                            */
-  ACP_SUM = 4u        /* decoded gradient = sum over workers (default: / p)   */
+  ACP_SUM = 4u,       /* decoded gradient = sum over workers (default: / p)   */
+  ACP_POWERSGD = 8u   /* run the Power-SGD baseline instead (Alg. 1;
+                         NEXT-1): each step projects twice, P = M'Q -> AR(P) ->
+                         orth(P) -> Q = M'^T P -> AR(Q), E = M' - P Q_loc^T,
+                         decoded = P Q^T / p. acp_step ignores parity; in the
+                         split API acp_compress(0) forms P (no orthogonalisation),
+                         acp_compress(1) orthogonalises the reduced P and forms
+                         Q, acp_decompress(1) decodes (acp_decompress(0) is a
+                         no-op). Needs error feedback and rank <= 8; not
+                         combinable with ACP_NO_EF / ACP_NO_REUSE            */
 };
 
 typedef struct {

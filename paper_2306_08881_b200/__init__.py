@@ -4,7 +4,7 @@ The compute path is ``lib/libacp.so`` (sm_100a kernels + NCCL) behind the C
 ABI in ``include/acp.h``; this package only marshals arguments. Importing it
 loads the library and fails loudly if it has not been built.
 """
-from ._lib import (load as _load, AcpError, ACP_NO_EF, ACP_NO_REUSE, ACP_SUM,  # noqa: F401
+from ._lib import (load as _load, AcpError, ACP_NO_EF, ACP_NO_REUSE, ACP_SUM, ACP_POWERSGD,  # noqa: F401
                    LIB_PATH, EXPORTED)
 from .acp import (AcpContext, nccl_comm_from_group, nccl_comm_destroy, broadcast_unique_id,  # noqa: F401
                   DEFAULT_BUCKET_BYTES)

@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "lib", "libacp.so")
 
 ACP_OK, ACP_E_INVAL, ACP_E_CUDA, ACP_E_NCCL, ACP_E_NOMEM, ACP_E_STATE = range(6)
-ACP_NO_EF, ACP_NO_REUSE, ACP_SUM = 1, 2, 4
+ACP_NO_EF, ACP_NO_REUSE, ACP_SUM, ACP_POWERSGD = 1, 2, 4, 8
 ACP_ABI_VERSION = 1
 (ACP_K_ORTH, ACP_K_PROJ_P, ACP_K_PROJ_Q, ACP_K_DECODE_P, ACP_K_DECODE_Q,
  ACP_K_ALLREDUCE) = range(6)

@@ -59,6 +59,7 @@ struct Plan {
   int T = 0, RT = 1, nsm = 148, nmat = 0;
   bool ef = true;
   bool defer = false;   // deferred Q-step residual (stream kernels)
+  bool psgd = false;    // ACP_POWERSGD: the Power-SGD baseline (NEXT-1)
   std::vector<LayerDesc> L;
   int64_t N = 0, e_elems = 0, arena[2] = {0, 0}, ql_elems = 0, wmat_elems = 0;
   std::vector<std::vector<int>> buckets[2];
@@ -145,6 +146,9 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
   P.nsm = nsm;
   P.T = cfg->num_tensors;
   P.ef = !(cfg->flags & ACP_NO_EF);
+  P.psgd = (cfg->flags & ACP_POWERSGD) != 0;
+  if (P.psgd && (cfg->flags & (ACP_NO_EF | ACP_NO_REUSE)))
+    return fail(ACP_E_INVAL, "ACP_POWERSGD cannot be combined with ACP_NO_EF / ACP_NO_REUSE");
   P.L.assign(P.T, LayerDesc{});
   int rmax = 1;
   for (int i = 0; i < P.T; ++i) {
@@ -365,7 +369,8 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
         bytes += 8.0 * L.n;
         continue;
       }
-      const double bpe = mode == 0 ? 12.0 : (mode == 2 ? 16.0 : (P.defer ? 12.0 : 8.0));
+      const double bpe = mode == 0 ? (P.psgd ? 8.0 : 12.0)
+                                   : (mode == 2 ? 16.0 : (P.defer ? 12.0 : 8.0));
       const StreamMap& mp = L.sm[mi];
       const bool fast = mp.tr > 0;
       const int64_t tr = fast ? mp.tr : 1;
@@ -404,6 +409,7 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
     if (stream_smem_bytes(ln.stages, ln.stage_floats, ln.factor_floats, ln.ptile) > 227 * 1024)
       smem_overflow = true;
     ln.defer = (P.defer && (mode == 0 || mode == 3)) ? 1 : 0;
+    if (P.psgd && mode == 0) ln.defer = 2;  // projection only (no residual write)
     int64_t part = 0;
     int prev_layer = -1, prev_panel = -1;
     ln.red_off = (int64_t)P.redtasks.size();
@@ -452,12 +458,15 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
   const bool use_stream = P.ef && P.RT <= 8;
   // the deferred Q-step residual needs the stream kernels' layouts; the
   // environment switch keeps the 24-B/element Q-step for comparison
-  P.defer = use_stream && !std::getenv("ACP_NO_DEFER");
+  P.defer = use_stream && !P.psgd && !std::getenv("ACP_NO_DEFER");
+  if (P.psgd && !use_stream)
+    return fail(ACP_E_INVAL, "ACP_POWERSGD needs error feedback and rank <= 8");
   auto k1_launch = [&](int parity, const std::vector<int>& ts) {
     if (use_stream) return stream_launch(parity == 0 ? 0 : 3, ts);
     return parity == 0 ? row_launch(0, ts) : col_launch(ts);
   };
   auto k3_launch = [&](int parity, const std::vector<int>& ts) {
+    if (P.psgd && parity == 0) return Launch{};  // Power-SGD decodes once, after Q
     if (parity == 1 && P.defer) return row_launch(3, ts);  // decode only
     if (parity == 1 && use_stream) return stream_launch(2, ts);
     return row_launch(parity == 0 ? 1 : 2, ts);
@@ -875,17 +884,11 @@ acp_status before_k1(acp_ctx* c, int32_t parity, cudaStream_t s) {
 }
 void after_k1(acp_ctx* c, int32_t parity) { c->e_deferred = c->P.defer && parity == 1; }
 
-// Enqueue one whole step (orthogonalise, per-bucket projection + all-reduce,
-// decode) on stream s; used eagerly and for graph capture.
-acp_status enqueue_step(acp_ctx* c, int32_t parity, cudaStream_t s) {
+// Per compute group: projection K1 of `parity` on s, then the group's buckets
+// all-reduced as one NCCL group on the comm stream (event ev_ar[g] marks it).
+acp_status project_and_reduce(acp_ctx* c, int32_t parity, cudaStream_t s) {
   acp_status st;
-  if ((st = run_orth(c, parity, s)) != ACP_OK) return st;
   const Plan& P = c->P;
-  if (c->cfg.world_size == 1) {
-    if ((st = run_k1(c, parity, P.k1_all[parity], s)) != ACP_OK) return st;
-    if ((st = run_k3(c, parity, P.k3_all[parity], s)) != ACP_OK) return st;
-    return ACP_OK;
-  }
   float* buf = parity == 0 ? c->tab.pbuf : c->tab.qbuf;
   const size_t ng = P.groups[parity].size();
   for (size_t g = 0; g < ng; ++g) {
@@ -909,7 +912,46 @@ acp_status enqueue_step(acp_ctx* c, int32_t parity, cudaStream_t s) {
     }
     CK(c, cudaEventRecord(c->ev_ar[g], c->comm_stream), "event record");
   }
-  for (size_t g = 0; g < ng; ++g) {
+  return ACP_OK;
+}
+
+// Power-SGD step (ACP_POWERSGD): P = M'Q -> AR(P) -> orth(P) ->
+// Q = M'^T P -> AR(Q) -> E = M' - P Q_loc^T, decoded = P Q^T / p.
+acp_status enqueue_psgd_step(acp_ctx* c, cudaStream_t s) {
+  acp_status st;
+  const Plan& P = c->P;
+  if (c->cfg.world_size == 1) {
+    if ((st = run_k1(c, 0, P.k1_all[0], s)) != ACP_OK) return st;
+    if ((st = run_orth(c, 1, s)) != ACP_OK) return st;
+    if ((st = run_k1(c, 1, P.k1_all[1], s)) != ACP_OK) return st;
+    return run_k3(c, 1, P.k3_all[1], s);
+  }
+  if ((st = project_and_reduce(c, 0, s)) != ACP_OK) return st;
+  for (size_t g = 0; g < P.groups[0].size(); ++g)
+    CK(c, cudaStreamWaitEvent(s, c->ev_ar[g], 0), "stream wait");
+  if ((st = run_orth(c, 1, s)) != ACP_OK) return st;  // needs every reduced P
+  if ((st = project_and_reduce(c, 1, s)) != ACP_OK) return st;
+  for (size_t g = 0; g < P.groups[1].size(); ++g) {
+    CK(c, cudaStreamWaitEvent(s, c->ev_ar[g], 0), "stream wait");
+    if ((st = run_k3(c, 1, P.k3_g[1][g], s)) != ACP_OK) return st;
+  }
+  return ACP_OK;
+}
+
+// Enqueue one whole step (orthogonalise, per-bucket projection + all-reduce,
+// decode) on stream s; used eagerly and for graph capture.
+acp_status enqueue_step(acp_ctx* c, int32_t parity, cudaStream_t s) {
+  if (c->P.psgd) return enqueue_psgd_step(c, s);
+  acp_status st;
+  if ((st = run_orth(c, parity, s)) != ACP_OK) return st;
+  const Plan& P = c->P;
+  if (c->cfg.world_size == 1) {
+    if ((st = run_k1(c, parity, P.k1_all[parity], s)) != ACP_OK) return st;
+    if ((st = run_k3(c, parity, P.k3_all[parity], s)) != ACP_OK) return st;
+    return ACP_OK;
+  }
+  if ((st = project_and_reduce(c, parity, s)) != ACP_OK) return st;
+  for (size_t g = 0; g < P.groups[parity].size(); ++g) {
     CK(c, cudaStreamWaitEvent(s, c->ev_ar[g], 0), "stream wait");
     if ((st = run_k3(c, parity, P.k3_g[parity][g], s)) != ACP_OK) return st;
   }
@@ -949,6 +991,7 @@ acp_status acp_step(acp_ctx* c, int32_t parity, float* const* grads, void* strea
   DeviceGuard dg(c->cfg.device);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if ((st = set_grads(c, grads, s)) != ACP_OK) return st;
+  if (c->P.psgd) parity = 0;  // one Power-SGD step does both projections
   if ((st = before_k1(c, parity, s)) != ACP_OK) return st;
   if (c->use_graphs && !c->profile) {
     if (!c->gexec[parity] && (st = capture_step(c, parity)) != ACP_OK) return st;
@@ -978,7 +1021,8 @@ acp_status acp_compress(acp_ctx* c, int32_t parity, float* const* grads, float**
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if ((st = set_grads(c, grads, s)) != ACP_OK) return st;
   if ((st = before_k1(c, parity, s)) != ACP_OK) return st;
-  if ((st = run_orth(c, parity, s)) != ACP_OK) return st;
+  // Power-SGD's first projection uses the previous Q as it is
+  if (!(c->P.psgd && parity == 0) && (st = run_orth(c, parity, s)) != ACP_OK) return st;
   if ((st = run_k1(c, parity, c->P.k1_all[parity], s)) != ACP_OK) return st;
   after_k1(c, parity);
   *out_buffer = parity == 0 ? c->tab.pbuf : c->tab.qbuf;

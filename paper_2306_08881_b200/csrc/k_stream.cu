@@ -235,7 +235,7 @@ __device__ void producer(const Tables& t, const StreamSeg* segs, int sb, int se,
 // ---------------------------------------------------------------------------
 template <int RT, int NC>
 __device__ void seg_k1p(const Tables& t, const LayerDesc& L, const StreamSeg& s,
-                        const Shared& sh, Pipe& pp, int& rph, int defer) {
+                        const Shared& sh, Pipe& pp, int& rph, int defer, int projonly) {
   constexpr int NW = Cfg<0>::NW;
   const StreamMap mp = L.sm[0];
   const int lg = mp.lg, gw = mp.gw, rs = mp.rs, TR = mp.tr;
@@ -355,14 +355,16 @@ __device__ void seg_k1p(const Tables& t, const LayerDesc& L, const StreamSeg& s,
         for (int k = 0; k < RT; ++k) acc[k] = __shfl_sync(0xffffffffu, tot, k);
       }
       const int64_t row = r0 + tri;
+      if (!projonly) {
 #pragma unroll
-      for (int i = 0; i < NC; ++i) {
-        float4 e;
-        if constexpr (kReload) e = corrected(tM, tE, toff, i, po);
-        else e = x[i];
+        for (int i = 0; i < NC; ++i) {
+          float4 e;
+          if constexpr (kReload) e = corrected(tM, tE, toff, i, po);
+          else e = x[i];
 #pragma unroll
-        for (int k = 0; k < RT; ++k) f4fma(e, -acc[k], qa[i][k]);
-        if (rval && cval[i]) st_cs4(E + row * m + coff[i], e);
+          for (int k = 0; k < RT; ++k) f4fma(e, -acc[k], qa[i][k]);
+          if (rval && cval[i]) st_cs4(E + row * m + coff[i], e);
+        }
       }
       if (kReload && j == rs - 1) {
         __syncwarp();
@@ -668,6 +670,8 @@ __device__ void seg_generic(const Tables& t, const LayerDesc& L, const StreamSeg
     }
     return;
   }
+  const int projonly = (MODE == 0) && (defer & 2);  // Power-SGD: no residual here
+  defer &= 1;
   for (int64_t row = s.row0 + warp; row < s.row1; row += NWc) {
     float* __restrict__ gr = grad + row * m;
     float* __restrict__ er = E + row * m;
@@ -693,7 +697,7 @@ __device__ void seg_generic(const Tables& t, const LayerDesc& L, const StreamSeg
       for (int off = 16; off > 0; off >>= 1)
 #pragma unroll
         for (int k = 0; k < RT; ++k) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], off);
-      for (int64_t j = lane; j < m; j += 32) {
+      for (int64_t j = lane; j < m && !projonly; j += 32) {
         float x = gr[j] + er[j];
         if (defer) {
 #pragma unroll
@@ -754,7 +758,7 @@ __global__ void __launch_bounds__(Cfg<MODE>::NW * 32 + 32, Cfg<MODE>::CPS)
   sh.flag = reinterpret_cast<int*>(sh.sP + (size_t)stages * ptile);
   // the producer warp stages P rows (32 cp.async arrivals per tile) for the
   // Q-step kernels and, when the residual is deferred, for the P-step one
-  const int stage_p = (ptile > 0) && (MODE != 0 || (defer && *t.deferred));
+  const int stage_p = (ptile > 0) && (MODE != 0 || ((defer & 1) && *t.deferred));
   if (threadIdx.x == 0) {
     for (int i = 0; i < stages; ++i) {
       mbar_init(&sh.full[i], stage_p ? 33 : 1);
@@ -766,6 +770,10 @@ __global__ void __launch_bounds__(Cfg<MODE>::NW * 32 + 32, Cfg<MODE>::CPS)
   const int sb = cta_begin[blockIdx.x], se = cta_begin[blockIdx.x + 1];
   // deferred Q-step residual: K1 Q-step raises the flag (nothing in that
   // launch reads it); K1 P-step reads it (cleared later by the P decode)
+  // defer bit 1 (mode 0): projection only, no residual (Power-SGD, whose
+  // residual is formed after the second projection)
+  const int projonly = (MODE == 0) && (defer & 2);
+  defer &= 1;
   int dflag = 0;
   if (MODE == 3 && defer && blockIdx.x == 0 && threadIdx.x == 0) *t.deferred = 1;
   if (MODE == 0 && defer) dflag = *t.deferred;
@@ -793,13 +801,13 @@ __global__ void __launch_bounds__(Cfg<MODE>::NW * 32 + 32, Cfg<MODE>::CPS)
       continue;
     }
     if (!is_fast<MODE>(L, grad)) {
-      seg_generic<MODE, RT>(t, L, s, grad, scale, sh.gred, MODE == 0 ? dflag : defer);
+      seg_generic<MODE, RT>(t, L, s, grad, scale, sh.gred, MODE == 0 ? (dflag | (projonly << 1)) : defer);
     } else {
       switch (L.sm[ModeIdx<MODE>::v].nc) {
 #define ACP_CASE(NCV)                                                            \
   case NCV:                                                                      \
     if constexpr (NCV <= nc_max(MODE, RT)) {                                     \
-      if constexpr (MODE == 0) seg_k1p<RT, NCV>(t, L, s, sh, pp, rph, dflag);    \
+      if constexpr (MODE == 0) seg_k1p<RT, NCV>(t, L, s, sh, pp, rph, dflag, projonly); \
       else seg_fast<MODE, RT, NCV>(t, L, s, grad, scale, sh, pp, rph, defer);   \
     }                                                                            \
     break;

@@ -19,7 +19,7 @@ import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
 from acp_harness import make_inputs, make_q0, TOL  # noqa: E402
-from oracle import AcpOracle, rel_frobenius  # noqa: E402
+from oracle import AcpOracle, PowerSgdOracle, rel_frobenius  # noqa: E402
 
 
 def main():
@@ -27,7 +27,8 @@ def main():
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     rank, world = dist.get_rank(), dist.get_world_size()
-    from paper_2306_08881_b200 import AcpContext, nccl_comm_from_group, nccl_comm_destroy
+    from paper_2306_08881_b200 import (AcpContext, nccl_comm_from_group, nccl_comm_destroy,
+                                       ACP_POWERSGD)
     comm = nccl_comm_from_group()
     seed = 2306088
     shapes = [(1000,), (64, 3, 7, 7), (2, 1024), (300, 1152), (17,), (512, 4608), (130, 20),
@@ -37,10 +38,12 @@ def main():
     inputs = make_inputs(shapes, world, steps, seed, "lowrank")
     q0 = make_q0(shapes, rank_r, seed)
     worst = 0.0
-    for bucket_bytes in (25 * 2 ** 20, 0, -1):   # paper rule, one tensor per bucket, one bucket
+    # paper rule, one tensor per bucket, one bucket; then the Power-SGD baseline
+    for bucket_bytes, flags in ((25 * 2 ** 20, 0), (0, 0), (-1, 0), (25 * 2 ** 20, ACP_POWERSGD)):
         ctx = AcpContext(shapes, rank_r, world_size=world, nccl_comm=comm, seed=seed, q0=q0,
-                         bucket_bytes=bucket_bytes)
-        o = AcpOracle(shapes, rank_r, world_size=world, seed=seed, q0=q0)
+                         bucket_bytes=bucket_bytes, flags=flags)
+        oc = PowerSgdOracle if flags else AcpOracle
+        o = oc(shapes, rank_r, world_size=world, seed=seed, q0=q0)
         for t in range(steps):
             g = [torch.from_numpy(np.ascontiguousarray(x)).cuda() for x in inputs[t][rank]]
             ctx.step(g, t % 2)
