@@ -205,6 +205,11 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
       // TMA stream kernels: thread mapping per mode (tr == 0: generic path)
       if (P.ef) {
         stream_make_map(0, L.m, P.RT, &L.sm[0]);
+        // K1-P stages the layer's local Q (RT x m) next to two ring stages
+        const StreamMap& m0 = L.sm[0];
+        if (m0.tr > 0 && 4 * ((int64_t)P.RT * L.m + 4LL * m0.tr * m0.pcols + 2LL * m0.tr * P.RT) +
+                                 24 * 1024 > 227 * 1024)
+          L.sm[0] = StreamMap{};  // generic path
         stream_make_map(2, L.m, P.RT, &L.sm[1]);
         stream_make_map(3, L.m, P.RT, &L.sm[2]);
       }

@@ -37,14 +37,22 @@ namespace {
 template <int MODE>
 struct Cfg;
 // K1 P-step: factor in registers (nc*RT float4)
+// (NW here is the r = 8 count; r <= 4 runs 12 consumer warps: nw_of)
 template <> struct Cfg<0> { static constexpr int NW = 8, CPS = 1, TT = 8192; };
 // K3 Q-step: two factors in registers (2*nc*RT float4), no barriers
 template <> struct Cfg<2> { static constexpr int NW = 8, CPS = 1, TT = 4096; };
 // K1 Q-step: accumulators nc*RT float4 in registers
 template <> struct Cfg<3> { static constexpr int NW = 8, CPS = 1, TT = 8192; };
 
+// Consumer warps per CTA. K1-P at r <= 4: 12 warps (13 with the producer ->
+// at most 4 per SM sub-partition -> 128 registers, nc <= 3): measured 0.87 ms
+// vs 0.96 ms with 8 warps x 168 registers on BERT-L (latency-bound loop).
+__host__ __device__ constexpr int nw_of(int mode, int RT) {
+  return (mode == 0 && RT <= 4) ? 12 : 8;
+}
+
 __host__ __device__ constexpr int nc_max(int mode, int RT) {
-  return mode == 0 ? (RT <= 4 ? 5 : (RT == 8 ? 4 : 0))
+  return mode == 0 ? (RT <= 4 ? 3 : (RT == 8 ? 4 : 0))
                    : (mode == 2 ? (RT <= 4 ? 3 : (RT == 8 ? 1 : 0)) : (RT <= 4 ? 4 : (RT == 8 ? 2 : 0)));
 }
 
@@ -236,7 +244,7 @@ __device__ void producer(const Tables& t, const StreamSeg* segs, int sb, int se,
 template <int RT, int NC>
 __device__ void seg_k1p(const Tables& t, const LayerDesc& L, const StreamSeg& s,
                         const Shared& sh, Pipe& pp, int& rph, int defer, int projonly) {
-  constexpr int NW = Cfg<0>::NW;
+  constexpr int NW = nw_of(0, RT);
   const StreamMap mp = L.sm[0];
   const int lg = mp.lg, gw = mp.gw, rs = mp.rs, TR = mp.tr;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -387,7 +395,7 @@ template <int MODE, int RT, int NC>
 __device__ void seg_fast(const Tables& t, const LayerDesc& L, const StreamSeg& s,
                          float* __restrict__ grad, float scale, const Shared& sh, Pipe& pp,
                          int& rph, int defer) {
-  constexpr int NW = Cfg<MODE>::NW;
+  constexpr int NW = nw_of(MODE, RT);
   const StreamMap mp = L.sm[ModeIdx<MODE>::v];
   const int lg = mp.lg, gw = mp.gw, rs = mp.rs, TR = mp.tr;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -620,7 +628,7 @@ __device__ void seg_generic(const Tables& t, const LayerDesc& L, const StreamSeg
   // row, lanes stride the columns, warp-shuffle row sums) so a layer with many
   // short rows does not serialise on CTA barriers; the column reduction
   // (mode 3) gives each thread a column and unrolls its row loop.
-  constexpr int NWc = Cfg<MODE>::NW;
+  constexpr int NWc = nw_of(MODE, RT);
   constexpr int NT = NWc * 32;
   (void)red;
   const int64_t m = L.m, n = L.n;
@@ -736,11 +744,11 @@ __device__ void seg_generic(const Tables& t, const LayerDesc& L, const StreamSeg
 }
 
 template <int MODE, int RT>
-__global__ void __launch_bounds__(Cfg<MODE>::NW * 32 + 32, Cfg<MODE>::CPS)
+__global__ void __launch_bounds__(nw_of(MODE, RT) * 32 + 32, Cfg<MODE>::CPS)
     stream_kernel(Tables t, const StreamSeg* __restrict__ segs, const int32_t* __restrict__ cta_begin,
                   float scale, int stages, int stage_floats, int factor_floats, int defer,
                   int ptile) {
-  constexpr int NT = Cfg<MODE>::NW * 32;
+  constexpr int NT = nw_of(MODE, RT) * 32;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Shared sh;
   sh.stages = stages;
@@ -762,7 +770,7 @@ __global__ void __launch_bounds__(Cfg<MODE>::NW * 32 + 32, Cfg<MODE>::CPS)
   if (threadIdx.x == 0) {
     for (int i = 0; i < stages; ++i) {
       mbar_init(&sh.full[i], stage_p ? 33 : 1);
-      mbar_init(&sh.empty[i], Cfg<MODE>::NW);
+      mbar_init(&sh.empty[i], nw_of(MODE, RT));
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -777,7 +785,7 @@ __global__ void __launch_bounds__(Cfg<MODE>::NW * 32 + 32, Cfg<MODE>::CPS)
   int dflag = 0;
   if (MODE == 3 && defer && blockIdx.x == 0 && threadIdx.x == 0) *t.deferred = 1;
   if (MODE == 0 && defer) dflag = *t.deferred;
-  if ((threadIdx.x >> 5) == Cfg<MODE>::NW) {  // producer warp
+  if ((threadIdx.x >> 5) == nw_of(MODE, RT)) {  // producer warp
     producer<MODE>(t, segs, sb, se, sh, stage_p);
     return;
   }
@@ -831,8 +839,8 @@ cudaError_t launch_mode(int rt, const Tables& t, const StreamSeg* segs, const in
   auto go = [&](auto kern) -> cudaError_t {
     cudaError_t e = allow_max_smem(reinterpret_cast<const void*>(kern));
     if (e != cudaSuccess) return e;
-    kern<<<ncta, Cfg<MODE>::NW * 32 + 32, smem, st>>>(t, segs, cb, scale, stages, stage_floats,
-                                                      factor_floats, defer, ptile);
+    kern<<<ncta, nw_of(MODE, rt) * 32 + 32, smem, st>>>(t, segs, cb, scale, stages, stage_floats,
+                                                        factor_floats, defer, ptile);
     return cudaGetLastError();
   };
   switch (rt) {
@@ -937,8 +945,10 @@ int stream_ctas_per_sm(int mode) {
 bool stream_make_map(int mode, int64_t m, int rt, StreamMap* out) {
   *out = StreamMap{};
   if (m % 4 != 0 || rt > 8) return false;
-  const int NW = mode == 0 ? Cfg<0>::NW : (mode == 2 ? Cfg<2>::NW : Cfg<3>::NW);
-  const int64_t TT = mode == 0 ? Cfg<0>::TT : (mode == 2 ? Cfg<2>::TT : Cfg<3>::TT);
+  const int NW = nw_of(mode, rt);
+  // K1-P at r = 8 stages an 8 x m local factor: halve its tiles to stay in 227 KB
+  const int64_t TT = mode == 0 ? (rt >= 8 ? Cfg<0>::TT / 2 : Cfg<0>::TT)
+                               : (mode == 2 ? Cfg<2>::TT : Cfg<3>::TT);
   const int ncm = nc_max(mode, rt);
   if (ncm <= 0) return false;
   const int64_t m4 = m / 4;
@@ -964,7 +974,8 @@ bool stream_make_map(int mode, int64_t m, int rt, StreamMap* out) {
     out->tr = (int32_t)(nrs * rs);
     return true;
   }
-  for (int gw = 1; gw <= NW; gw <<= 1) {
+  for (int gw = 1; gw <= NW; ++gw) {
+    if (NW % gw) continue;  // gw warps per row, NW / gw row groups
     const int64_t nc = (pc4 + 32LL * gw - 1) / (32LL * gw);
     if (nc > ncm) continue;
     const int64_t nrs = NW / gw;
