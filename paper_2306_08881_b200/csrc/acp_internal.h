@@ -2,6 +2,7 @@
 // sm_100a kernels. Not part of the ABI.
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace acp {
@@ -26,6 +27,14 @@ struct StreamMap {
   int16_t np, pad_;
 };
 
+// Tensor-core K1 Q-step mapping of one layer (k_tc.cu): column panels of pc
+// columns (multiple of 16), warps = wc column groups (cbw 16-column blocks
+// each) x wr row groups; tiles of tr rows; each segment writes wr partial slots.
+struct TcMap {
+  int32_t pc;
+  int16_t np, wc, wr, tr, cbw, pad_;
+};
+
 // Per-tensor descriptor uploaded once (device copy of the plan).
 struct LayerDesc {
   int64_t n, m;        // matrix n x m; vector: n = length, m = 0
@@ -43,6 +52,22 @@ struct LayerDesc {
   int32_t deg_idx;     // K2: index into the degenerate-mask / counter arrays
   int32_t pad_;
   StreamMap sm[3];     // stream kernels: [0] K1 P-step, [1] K3 Q-step, [2] K1 Q-step
+  int64_t qs_off;      // TC path: offset of the layer's [2][R8][m] Q-side split factors
+  int64_t ps_off;      // TC path: offset of the layer's [2][n][R8] P-side split factors
+  TcMap tq;            // TC path: K1 Q-step mapping
+};
+
+// Tensor-core K1 work unit (k_tc.cu): rows [row0, row1) of matrix `layer`
+// (column panel `panel` on Q-steps), or elements of a vector (packed).
+// Q-steps: the segment writes nslot partial slots (r x pc floats, k-major,
+// stride round4(r * pc)) starting at part_off.
+struct TcSeg {
+  int32_t layer;
+  int32_t panel;
+  int64_t row0, row1;
+  int64_t part_off;
+  int32_t nslot;
+  int32_t pad_;
 };
 
 // Stream-kernel work unit: rows [row0, row1) of matrix `layer` (or elements of
@@ -105,6 +130,8 @@ struct ColReduceTask {
   int64_t cols;         // columns of this panel
   int64_t m;            // layer width (Q slot row length)
   int64_t q_dst, ql_dst;  // float offsets of column c0 of k-row 0 in the Q-buffer / local-Q copy
+  int64_t qs_dst;       // TC path: offset of column c0 in the Q_loc split array (-1: none)
+  int64_t qs_lo;        // TC path: offset of the lo half (R8 * m)
   int32_t pcount;       // partial slots of the unit
   int32_t item_begin, item_end;
   int32_t pad_;
@@ -126,6 +153,15 @@ struct Tables {
   int64_t* step;         // device step counter (keys the method's random draws)
   int32_t* deferred;     // 1: E holds S = M' of the last Q-step (E = S - P Q_loc^T
                          //    is applied lazily by the next P-step), 0: E is materialised
+  // tensor-core path (double-deferred residual): 3xTF32 split
+  // copies (hi, lo) of the factors, ranks padded to r8 with zeros
+  float* qsplit;         // Q_orth  [2][R8][m] per layer (written by K2, side 0)
+  float* qlsplit;        // Q_loc   [2][R8][m] (written by the Q-step column reduce)
+  float* psplit;         // P_orth  [2][n][R8] (written by K2, side 1)
+  float* plsplit;        // P_loc   [2][n][R8] (written by the P-step TC kernel)
+  int32_t r8;            // padded rank (multiple of 8), 0: TC path off
+  const CUtensorMap* tmaps;  // TC path: per layer [M, S, Q_orth hi, lo, Q_loc hi, lo] (P-step
+                             // boxes) + [M, S] (Q-step boxes of tq.tr rows): 8 2-D TMA maps
 };
 
 // launches (all on `stream`, 256 threads, grid = ncta)
@@ -158,6 +194,22 @@ cudaError_t launch_stream(int mode, int rt, const Tables& t, const StreamSeg* se
 cudaError_t launch_materialize(const Tables& t, const LayerDesc& L, int layer, float* dst,
                                cudaStream_t stream);
 bool stream_make_map(int mode, int64_t m, int rt, StreamMap* out);
+// Tensor-core K1 (k_tc.cu). mode 0: P-step (x = M + S - P_orth Q_loc^T,
+// S = x, P_loc = x Q_orth -> P slot + P_loc split), mode 1: Q-step
+// (x = M + S - P_loc Q_orth^T, S = x, Q partials = x^T P_orth -> colpart).
+cudaError_t launch_tc(int mode, int r8, const Tables& t, const TcSeg* segs, const int32_t* cta_begin,
+                      int ncta, int stages, int stage_floats, cudaStream_t stream);
+size_t tc_smem_bytes(int stages, int stage_floats);
+// host: encode a 2-D TMA map (fp32 rows x cols, 32-column boxes of box_rows
+// rows, SWIZZLE_128B); false (map zeroed) when the layout does not allow it
+bool tc_encode_map(CUtensorMap* out, const float* base, int64_t cols, int64_t rows, int box_rows);
+int tc_p_box_rows();
+int tc_p_stage_floats(int r8);
+// K1 Q-step tile geometry of an m-column layer; returns stage floats
+int tc_q_map(int64_t m, int r8, TcMap* out);
+// TC state -> E: dst = S - A B^T (which 1: A = P_orth, B = Q_loc; 2: A = P_loc, B = Q_orth)
+cudaError_t launch_tc_materialize(const Tables& t, const LayerDesc& L, int which, float* dst,
+                                  cudaStream_t stream);
 int stream_ctas_per_sm(int mode);
 size_t stream_smem_bytes(int stages, int stage_floats, int factor_floats, int ptile);
 // K2: CholeskyQR2 of the factors named by segs (side 0: Q factors in the

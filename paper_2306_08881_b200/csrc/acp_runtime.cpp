@@ -36,7 +36,8 @@ inline size_t align256(size_t x) { return (x + 255) / 256 * 256; }
 constexpr int kMaxRank = 32;
 
 struct Launch {
-  int kind = 0;          // 0 register row kernel, 1 register col kernel, 2 TMA stream kernel
+  int kind = 0;          // 0 register row kernel, 1 register col kernel, 2 TMA stream kernel,
+                         // 3 tensor-core K1 (k_tc.cu; mode 0 P-step, 1 Q-step)
   int mode = 0;          // row: 0/1/2; stream: 0/2/3
   int64_t seg_off = 0;   // first segment (row, col or stream array)
   int64_t cb_off = 0;    // first entry of cta_begin
@@ -60,6 +61,10 @@ struct Plan {
   bool ef = true;
   bool defer = false;   // deferred Q-step residual (stream kernels)
   bool psgd = false;    // ACP_POWERSGD: the Power-SGD baseline (NEXT-1)
+  bool tc = false;      // tensor-core K1 + double-deferred residual
+  int R8 = 0;           // TC path: rank padded to a multiple of 8
+  int64_t qs_elems = 0, ps_elems = 0;  // TC path: split-factor array sizes (floats)
+  std::vector<TcSeg> tcsegs;
   std::vector<LayerDesc> L;
   int64_t N = 0, e_elems = 0, arena[2] = {0, 0}, ql_elems = 0, wmat_elems = 0;
   std::vector<std::vector<int>> buckets[2];
@@ -86,6 +91,8 @@ struct Plan {
          off_gram = 0, off_wmat = 0, off_orthcnt = 0, off_degmask = 0, off_layers = 0,
          off_grads = 0, off_rowsegs = 0, off_colsegs = 0, off_streamsegs = 0, off_orth[2] = {0, 0},
          off_ctab = 0, off_step = 0, off_red = 0, off_defer = 0,
+         off_qsplit = 0, off_qlsplit = 0, off_psplit = 0, off_plsplit = 0, off_tcsegs = 0,
+         off_tmaps = 0,
          total = 0;
 };
 
@@ -165,8 +172,15 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
     if (L.mat) ++P.nmat;
   }
   while (P.RT < rmax) P.RT <<= 1;
+  // tensor-core K1 with the double-deferred residual for r >= 8 (the SIMT
+  // stream kernels are faster at r <= 4); ACP_TC=1 / ACP_NO_TC=1 override
+  const char* tc_env = std::getenv("ACP_TC");
+  P.tc = P.ef && !P.psgd && P.RT <= 32 && !std::getenv("ACP_NO_TC") &&
+         (P.RT >= 8 || (tc_env && std::atoi(tc_env) != 0));
+  P.R8 = P.tc ? std::max(8, (P.RT + 7) / 8 * 8) : 0;
+  int tc_q_stage = 0;
   // offsets
-  int64_t e = 0, ql = 0, w = 0, so[2] = {0, 0};
+  int64_t e = 0, ql = 0, w = 0, so[2] = {0, 0}, qs = 0, ps = 0;
   for (int p = 0; p < 2; ++p) P.payload[p].resize(P.T);
   for (int i = 0; i < P.T; ++i) {
     LayerDesc& L = P.L[i];
@@ -200,6 +214,15 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
           }
         }
       }
+      L.qs_off = -1;
+      L.ps_off = -1;
+      if (P.tc) {
+        L.qs_off = qs;
+        qs += round4(2LL * P.R8 * L.m);
+        L.ps_off = ps;
+        ps += round4(2LL * P.R8 * L.n);
+        tc_q_stage = std::max(tc_q_stage, tc_q_map(L.m, P.R8, &L.tq));
+      }
       L.W = (L.m % 4 == 0 && P.RT <= 8) ? 4 : ((L.m % 2 == 0 && P.RT <= 16) ? 2 : 1);
       L.pw = kThreads * L.W;
       // TMA stream kernels: thread mapping per mode (tr == 0: generic path)
@@ -217,8 +240,12 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
       L.e_off = -1;
       L.ql_off = -1;
       L.w_off = -1;
+      L.qs_off = -1;
+      L.ps_off = -1;
     }
   }
+  P.qs_elems = qs;
+  P.ps_elems = ps;
   P.e_elems = e;
   P.ql_elems = ql;
   P.wmat_elems = std::max<int64_t>(w, 1);
@@ -442,6 +469,7 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
           tk.m = L.m;
           tk.q_dst = L.q_off + c0;
           tk.ql_dst = L.ql_off + c0;
+          tk.qs_dst = -1;
           tk.pcount = 0;
           tk.item_begin = ln.nitems;
           ln.nitems += (int)(L.r * ((tk.cols + 3) / 4));
@@ -463,15 +491,92 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
   const bool use_stream = P.ef && P.RT <= 8;
   // the deferred Q-step residual needs the stream kernels' layouts; the
   // environment switch keeps the 24-B/element Q-step for comparison
-  P.defer = use_stream && !P.psgd && !std::getenv("ACP_NO_DEFER");
+  P.defer = use_stream && !P.psgd && !P.tc && !std::getenv("ACP_NO_DEFER");
   if (P.psgd && !use_stream)
     return fail(ACP_E_INVAL, "ACP_POWERSGD needs error feedback and rank <= 8");
+  // tensor-core K1 launch (mode 0 P-step, 1 Q-step) over `tensors`
+  auto tc_launch = [&](int mode, const std::vector<int>& tensors) {
+    std::vector<Unit> units;
+    double bytes = 0;
+    for (int i : tensors) {
+      const LayerDesc& L = P.L[i];
+      if (!L.mat) {
+        units.push_back({i, -1, L.n, 8.0, 1024});
+        bytes += 8.0 * L.n;
+        continue;
+      }
+      // algorithmic bytes: M, S read, S written + the factors once
+      bytes += 12.0 * (double)L.n * (double)L.m + 4.0 * L.r * (2.0 * L.n + 2.0 * L.m);
+      if (mode == 0) {
+        units.push_back({i, -1, L.n, 12.0 * (double)L.m, 128});
+      } else {
+        for (int pn = 0; pn < L.tq.np; ++pn) {
+          const int64_t cols = std::min<int64_t>(L.tq.pc, L.m - (int64_t)pn * L.tq.pc);
+          units.push_back({i, pn, L.n, 12.0 * (double)cols, L.tq.tr});
+        }
+      }
+    }
+    Launch ln;
+    ln.kind = 3;
+    ln.mode = mode;
+    ln.seg_off = (int64_t)P.tcsegs.size();
+    ln.cb_off = (int64_t)P.ctab.size();
+    ln.stage_floats = std::max(4, mode == 0 ? tc_p_stage_floats(P.R8) : tc_q_stage);
+    ln.stages = (int)std::max<int64_t>(2, std::min<int64_t>(6, (200 * 1024) / (4LL * ln.stage_floats)));
+    if (tc_smem_bytes(ln.stages, ln.stage_floats) > 227 * 1024) smem_overflow = true;
+    int64_t part = 0;
+    int prev_layer = -1, prev_panel = -1;
+    ln.red_off = (int64_t)P.redtasks.size();
+    ln.ncta = split_units(units, min_share, nsm, P.ctab, [&](const Unit& u, int64_t a, int64_t b) {
+      TcSeg sg{};
+      sg.layer = u.layer;
+      sg.row0 = a;
+      sg.row1 = b;
+      sg.panel = u.panel < 0 ? 0 : u.panel;
+      const LayerDesc& L = P.L[u.layer];
+      if (mode == 1 && L.mat) {
+        const int64_t pc = L.tq.pc;
+        const int64_t stride = round4((int64_t)L.r * pc);
+        if (u.layer != prev_layer || u.panel != prev_panel) {
+          prev_layer = u.layer;
+          prev_panel = u.panel;
+          ColReduceTask tk{};
+          const int64_t c0 = (int64_t)sg.panel * pc;
+          tk.part_first = part;
+          tk.stride = stride;
+          tk.pc = pc;
+          tk.cols = std::min<int64_t>(pc, L.m - c0);
+          tk.m = L.m;
+          tk.q_dst = L.q_off + c0;
+          tk.ql_dst = L.ql_off + c0;
+          tk.qs_dst = L.qs_off + c0;
+          tk.qs_lo = (int64_t)P.R8 * L.m;
+          tk.pcount = 0;
+          tk.item_begin = ln.nitems;
+          ln.nitems += (int)(L.r * ((tk.cols + 3) / 4));
+          tk.item_end = ln.nitems;
+          P.redtasks.push_back(tk);
+          ++ln.nred;
+        }
+        sg.nslot = L.tq.wr;
+        sg.part_off = part;
+        part += (int64_t)L.tq.wr * stride;
+        P.redtasks.back().pcount += L.tq.wr;
+      }
+      P.tcsegs.push_back(sg);
+    });
+    if (mode == 1) P.colpart_elems = std::max(P.colpart_elems, part);
+    ln.bytes = bytes;
+    return ln;
+  };
   auto k1_launch = [&](int parity, const std::vector<int>& ts) {
+    if (P.tc) return tc_launch(parity, ts);
     if (use_stream) return stream_launch(parity == 0 ? 0 : 3, ts);
     return parity == 0 ? row_launch(0, ts) : col_launch(ts);
   };
   auto k3_launch = [&](int parity, const std::vector<int>& ts) {
     if (P.psgd && parity == 0) return Launch{};  // Power-SGD decodes once, after Q
+    if (P.tc) return row_launch(parity == 0 ? 1 : 3, ts);  // write-only decodes
     if (parity == 1 && P.defer) return row_launch(3, ts);  // decode only
     if (parity == 1 && use_stream) return stream_launch(2, ts);
     return row_launch(parity == 0 ? 1 : 2, ts);
@@ -565,6 +670,12 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
   P.off_orth[0] = take(sizeof(OrthSeg) * P.orthsegs[0].size());
   P.off_orth[1] = take(sizeof(OrthSeg) * P.orthsegs[1].size());
   P.off_ctab = take(4 * P.ctab.size());
+  P.off_qsplit = take(4 * (size_t)P.qs_elems);
+  P.off_qlsplit = take(4 * (size_t)P.qs_elems);
+  P.off_psplit = take(4 * (size_t)P.ps_elems);
+  P.off_plsplit = take(4 * (size_t)P.ps_elems);
+  P.off_tcsegs = take(sizeof(TcSeg) * P.tcsegs.size());
+  P.off_tmaps = take(P.tc ? sizeof(CUtensorMap) * 8 * (size_t)P.T : 0);
   P.off_step = take(8);
   P.off_defer = take(8);
   P.off_red = take(sizeof(ColReduceTask) * P.redtasks.size());
@@ -603,6 +714,8 @@ struct acp_ctx {
   std::vector<float*> grads_cache;
   int64_t step_count = 0;
   bool e_deferred = false;  // host mirror of *tab.deferred
+  int tc_state = 0;         // TC path: 0 E = S, 1 E = S - P_orth Q_loc^T, 2 E = S - P_loc Q_orth^T
+  std::vector<CUtensorMap> tmaps;  // TC path: host copy of the per-layer TMA maps
   int64_t launches = 0;
   bool poisoned = false;
   bool profile = false;
@@ -657,6 +770,9 @@ const ColSeg* dev_colsegs(acp_ctx* c, const Launch& ln) {
 const StreamSeg* dev_streamsegs(acp_ctx* c, const Launch& ln) {
   return reinterpret_cast<const StreamSeg*>(c->ws + c->P.off_streamsegs) + ln.seg_off;
 }
+const TcSeg* dev_tcsegs(acp_ctx* c, const Launch& ln) {
+  return reinterpret_cast<const TcSeg*>(c->ws + c->P.off_tcsegs) + ln.seg_off;
+}
 const int32_t* dev_ctab(acp_ctx* c, const Launch& ln) {
   return reinterpret_cast<const int32_t*>(c->ws + c->P.off_ctab) + ln.cb_off;
 }
@@ -670,7 +786,16 @@ acp_status run_k1(acp_ctx* c, int parity, const Launch& ln, cudaStream_t s) {
   const int ef = c->P.ef ? 1 : 0;
   ProfRec* r = prof_begin(c, parity == 0 ? ACP_K_PROJ_P : ACP_K_PROJ_Q, ln.bytes, s);
   cudaError_t e;
-  if (ln.kind == 2) {
+  if (ln.kind == 3) {
+    e = launch_tc(ln.mode, c->P.R8, c->tab, dev_tcsegs(c, ln), dev_ctab(c, ln), ln.ncta, ln.stages,
+                  ln.stage_floats, s);
+    if (e == cudaSuccess && ln.mode == 1 && ln.nred > 0) {
+      e = launch_col_reduce(c->tab,
+                            reinterpret_cast<const ColReduceTask*>(c->ws + c->P.off_red) + ln.red_off,
+                            ln.nred, ln.nitems, s);
+      ++c->launches;
+    }
+  } else if (ln.kind == 2) {
     e = launch_stream(ln.mode, c->P.RT, c->tab, dev_streamsegs(c, ln), dev_ctab(c, ln), ln.ncta,
                       1.0f, ln.stages, ln.stage_floats, ln.factor_floats, ln.defer, ln.ptile, s);
     if (e == cudaSuccess && ln.mode == 3 && ln.nred > 0) {
@@ -737,6 +862,30 @@ acp_status set_grads(acp_ctx* c, float* const* grads, cudaStream_t s) {
   // pageable source: staged before return, so the cache can change afterwards
   CK(c, cudaMemcpyAsync(c->ws + c->P.off_grads, c->grads_cache.data(), 8 * (size_t)c->P.T,
                         cudaMemcpyHostToDevice, s), "gradient table upload");
+  if (c->P.tc) {
+    // TC P-step: TMA maps of the gradients (M) next to the fixed ones (S, factors)
+    const Plan& P = c->P;
+    c->tmaps.resize(8 * (size_t)P.T);
+    for (int i = 0; i < P.T; ++i) {
+      const LayerDesc& L = P.L[i];
+      CUtensorMap* mp = c->tmaps.data() + 8 * (size_t)i;
+      if (!L.mat) {
+        std::memset(mp, 0, 8 * sizeof(CUtensorMap));
+        continue;
+      }
+      const int br = tc_p_box_rows();
+      tc_encode_map(mp + 0, c->grads_cache[i], L.m, L.n, br);
+      tc_encode_map(mp + 1, c->tab.E + L.e_off, L.m, L.n, br);
+      tc_encode_map(mp + 2, c->tab.qsplit + L.qs_off, L.m, P.R8, P.R8);
+      tc_encode_map(mp + 3, c->tab.qsplit + L.qs_off + (int64_t)P.R8 * L.m, L.m, P.R8, P.R8);
+      tc_encode_map(mp + 4, c->tab.qlsplit + L.qs_off, L.m, P.R8, P.R8);
+      tc_encode_map(mp + 5, c->tab.qlsplit + L.qs_off + (int64_t)P.R8 * L.m, L.m, P.R8, P.R8);
+      tc_encode_map(mp + 6, c->grads_cache[i], L.m, L.n, L.tq.tr);
+      tc_encode_map(mp + 7, c->tab.E + L.e_off, L.m, L.n, L.tq.tr);
+    }
+    CK(c, cudaMemcpyAsync(c->ws + P.off_tmaps, c->tmaps.data(), sizeof(CUtensorMap) * c->tmaps.size(),
+                          cudaMemcpyHostToDevice, s), "tensor map upload");
+  }
   return ACP_OK;
 }
 
@@ -806,6 +955,12 @@ acp_status acp_create(const acp_config* cfg, acp_ctx** out) {
   t.degmask = reinterpret_cast<uint32_t*>(c->ws + P.off_degmask);
   t.step = reinterpret_cast<int64_t*>(c->ws + P.off_step);
   t.deferred = reinterpret_cast<int32_t*>(c->ws + P.off_defer);
+  t.qsplit = reinterpret_cast<float*>(c->ws + P.off_qsplit);
+  t.qlsplit = reinterpret_cast<float*>(c->ws + P.off_qlsplit);
+  t.psplit = reinterpret_cast<float*>(c->ws + P.off_psplit);
+  t.plsplit = reinterpret_cast<float*>(c->ws + P.off_plsplit);
+  t.r8 = P.R8;
+  t.tmaps = reinterpret_cast<const CUtensorMap*>(c->ws + P.off_tmaps);
 
   DeviceGuard dg(cfg->device);
   cudaStream_t s = nullptr;
@@ -824,6 +979,7 @@ acp_status acp_create(const acp_config* cfg, acp_ctx** out) {
       (e = up(P.off_rowsegs, P.rowsegs.data(), sizeof(RowSeg) * P.rowsegs.size())) != cudaSuccess ||
       (e = up(P.off_colsegs, P.colsegs.data(), sizeof(ColSeg) * P.colsegs.size())) != cudaSuccess ||
       (e = up(P.off_streamsegs, P.streamsegs.data(), sizeof(StreamSeg) * P.streamsegs.size())) != cudaSuccess ||
+      (e = up(P.off_tcsegs, P.tcsegs.data(), sizeof(TcSeg) * P.tcsegs.size())) != cudaSuccess ||
       (e = up(P.off_orth[0], P.orthsegs[0].data(), sizeof(OrthSeg) * P.orthsegs[0].size())) != cudaSuccess ||
       (e = up(P.off_orth[1], P.orthsegs[1].data(), sizeof(OrthSeg) * P.orthsegs[1].size())) != cudaSuccess ||
       (e = up(P.off_ctab, P.ctab.data(), 4 * P.ctab.size())) != cudaSuccess ||
@@ -882,12 +1038,34 @@ acp_status materialize_all(acp_ctx* c, cudaStream_t s) {
   return ACP_OK;
 }
 
+// TC path: fold the implicit residual into S (state -> 0) and zero the split
+// factor the next K1's correction would pair with it (eager, irregular
+// parity sequences and set_state only; the steady state never needs it).
+acp_status tc_materialize_all(acp_ctx* c, cudaStream_t s) {
+  if (c->tc_state == 0) return ACP_OK;
+  for (int i = 0; i < c->P.T; ++i)
+    if (c->P.L[i].mat)
+      CK(c, launch_tc_materialize(c->tab, c->P.L[i], c->tc_state, nullptr, s), "materialize E");
+  CK(c, cudaMemsetAsync(c->tab.qlsplit, 0, 4 * (size_t)c->P.qs_elems, s), "zero Q_loc split");
+  CK(c, cudaMemsetAsync(c->tab.plsplit, 0, 4 * (size_t)c->P.ps_elems, s), "zero P_loc split");
+  c->tc_state = 0;
+  return ACP_OK;
+}
+
 // host bookkeeping before/after a K1 of `parity`
 acp_status before_k1(acp_ctx* c, int32_t parity, cudaStream_t s) {
+  if (c->P.tc) {  // P after P / Q after Q: the steady-state correction does not apply
+    if ((parity == 0 && c->tc_state == 2) || (parity == 1 && c->tc_state == 1))
+      return tc_materialize_all(c, s);
+    return ACP_OK;
+  }
   if (parity == 1 && c->e_deferred) return materialize_all(c, s);  // Q after Q
   return ACP_OK;
 }
-void after_k1(acp_ctx* c, int32_t parity) { c->e_deferred = c->P.defer && parity == 1; }
+void after_k1(acp_ctx* c, int32_t parity) {
+  c->e_deferred = c->P.defer && parity == 1;
+  if (c->P.tc) c->tc_state = parity == 0 ? 2 : 1;
+}
 
 // Per compute group: projection K1 of `parity` on s, then the group's buckets
 // all-reduced as one NCCL group on the comm stream (event ev_ar[g] marks it).
@@ -1056,7 +1234,9 @@ acp_status acp_get_state(acp_ctx* c, int32_t i, float* Pm, float* Qm, float* Em,
   if (Pm) CK(c, launch_transpose(c->tab.pbuf + L.p_off, Pm, L.n, L.r, 0, s), "state transpose");
   if (Qm) CK(c, launch_transpose(c->tab.qbuf + L.q_off, Qm, L.m, L.r, 0, s), "state transpose");
   if (Em) {
-    if (c->e_deferred)  // E = S - P Q_loc^T, formed on the fly (state unchanged)
+    if (c->P.tc && c->tc_state != 0)  // E = S - A B^T, formed on the fly (state unchanged)
+      CK(c, launch_tc_materialize(c->tab, L, c->tc_state, Em, s), "materialize E");
+    else if (c->e_deferred)  // E = S - P Q_loc^T, formed on the fly (state unchanged)
       CK(c, launch_materialize(c->tab, L, i, Em, s), "materialize E");
     else
       CK(c, cudaMemcpyAsync(Em, c->tab.E + L.e_off, 4 * (size_t)(L.n * L.m),
@@ -1074,6 +1254,7 @@ acp_status acp_set_state(acp_ctx* c, int32_t i, const float* Pm, const float* Qm
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const LayerDesc& L = c->P.L[i];
   if ((st = materialize_all(c, s)) != ACP_OK) return st;  // other layers keep their E
+  if ((st = tc_materialize_all(c, s)) != ACP_OK) return st;
   if (Pm) CK(c, launch_transpose(Pm, c->tab.pbuf + L.p_off, L.n, L.r, 1, s), "state transpose");
   if (Qm) CK(c, launch_transpose(Qm, c->tab.qbuf + L.q_off, L.m, L.r, 1, s), "state transpose");
   if (Em) CK(c, cudaMemcpyAsync(c->tab.E + L.e_off, Em, 4 * (size_t)(L.n * L.m),

@@ -85,6 +85,22 @@ __global__ void __launch_bounds__(kThreads) orth_kernel(Tables t, int side,
         }
         vf = (float)v;
         F[(int64_t)l * len + s.row0 + i] = vf;
+        if (phase == 2 && t.r8 > 0) {
+          // TC path: 3xTF32 split copies (Q side k-major [2][R8][m], P side
+          // row-major [2][n][R8]) for the tensor-core K1 kernels
+          uint32_t hi, lo;
+          split_tf32(vf, hi, lo);
+          const int64_t row = s.row0 + i, R8 = t.r8;
+          if (side == 0) {
+            float* d = t.qsplit + L.qs_off;
+            d[l * len + row] = __uint_as_float(hi);
+            d[(R8 + l) * len + row] = __uint_as_float(lo);
+          } else {
+            float* d = t.psplit + L.ps_off;
+            d[row * R8 + l] = __uint_as_float(hi);
+            d[(len + row) * R8 + l] = __uint_as_float(lo);
+          }
+        }
       }
       B[l * kLd + i] = vf;
     }

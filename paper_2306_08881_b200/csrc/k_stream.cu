@@ -56,66 +56,6 @@ __host__ __device__ constexpr int nc_max(int mode, int RT) {
                    : (mode == 2 ? (RT <= 4 ? 3 : (RT == 8 ? 1 : 0)) : (RT <= 4 ? 4 : (RT == 8 ? 2 : 0)));
 }
 
-__device__ __forceinline__ uint32_t s32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t cnt) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s32(b)), "r"(cnt) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_tx(uint64_t* b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s32(b)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-  uint32_t done;
-  do {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}\n"
-        : "=r"(done)
-        : "r"(s32(b)), "r"(parity)
-        : "memory");
-  } while (!done);
-}
-__device__ __forceinline__ bool mbar_test(uint64_t* b, uint32_t parity) {
-  uint32_t done;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-      "selp.u32 %0, 1, 0, p;\n\t}\n"
-      : "=r"(done)
-      : "r"(s32(b)), "r"(parity)
-      : "memory");
-  return done != 0;
-}
-__device__ __forceinline__ uint64_t policy_evict_first() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-// 1-D bulk copy global -> shared (TMA engine), completion counted on `bar`
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
-                                         uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1], %2, [%3], %4;" ::"r"(s32(dst)),
-      "l"(src), "r"(bytes), "r"(s32(bar)), "l"(policy)
-      : "memory");
-}
-// 4-byte async copy global -> shared (LDGSTS); src_bytes = 0 zero-fills
-__device__ __forceinline__ void cp_async4(float* dst, const float* src, uint32_t src_bytes) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(s32(dst)), "l"(src),
-               "r"(src_bytes)
-               : "memory");
-}
-// arrive on `bar` once all of this thread's prior cp.async have landed
-__device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared.b64 [%0];" ::"r"(s32(bar)) : "memory");
-}
 template <int NT>
 __device__ __forceinline__ void cta_sync1() {
   asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
@@ -873,7 +813,7 @@ __global__ void __launch_bounds__(256) col_reduce_kernel(Tables t, const ColRedu
   const int k = local / c4, c = (local - k * c4) * 4;
   const float* base = t.colpart + tk.part_first + (int64_t)k * tk.pc + c;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  const bool vec = (tk.cols & 3) == 0;
+  const bool vec = ((tk.cols | tk.m | tk.q_dst | tk.ql_dst) & 3) == 0;  // 16-byte aligned rows
   for (int p = j; p < tk.pcount; p += kSplit) {
     const float* src = base + (int64_t)p * tk.stride;
     if (vec) {
@@ -903,6 +843,16 @@ __global__ void __launch_bounds__(256) col_reduce_kernel(Tables t, const ColRedu
     for (int u = 0; u < 4 && c + u < tk.cols; ++u) {
       q[u] = v[u];
       ql[u] = v[u];
+    }
+  }
+  if (tk.qs_dst >= 0) {  // TC path: Q_loc split copy (k-major [2][R8][m])
+    float* d = t.qlsplit + tk.qs_dst + (int64_t)k * tk.m + c;
+    const float v[4] = {acc.x, acc.y, acc.z, acc.w};
+    for (int u = 0; u < 4 && c + u < tk.cols; ++u) {
+      uint32_t hi, lo;
+      split_tf32(v[u], hi, lo);
+      d[u] = __uint_as_float(hi);
+      d[tk.qs_lo + u] = __uint_as_float(lo);
     }
   }
 }

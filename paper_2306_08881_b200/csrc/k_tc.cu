@@ -1,0 +1,685 @@
+// Tensor-core K1 kernels with the double-deferred residual.
+//
+// Alg. 2 P:221-222 (P-step) and P:226-227 (Q-step) with the residual of each
+// step left implicit: after a step the error is E = S - A B^T, where S is the
+// step's input sum M' (written back into the E region) and (A, B) are the
+// step's local factor and the reused (orthogonalised) one. The next step
+// forms M' = M + E_prev = M + S - A B^T on the fly, writes it back as its own
+// S, and projects it:
+//
+//   mode 0, P-step:  x = M + S - P_orth Q_loc^T;  S <- x;  P_loc = x Q_orth
+//                    (P slot <- P_loc for the all-reduce; P_loc split kept)
+//   mode 1, Q-step:  x = M + S - P_loc Q_orth^T;  S <- x;  Q_loc = x^T P_orth
+//                    (per-segment partials; col_reduce_kernel sums them)
+//
+// so each K1 streams 12 B per element (read M, S; write S) and nothing has to
+// hold a whole row: the P-step's row sums accumulate across column panels.
+// Both rank-r products run on the tensor cores (mma.sync m16n8k8 TF32) in
+// 3xTF32 form, x = hi + lo, so the result keeps fp32-class accuracy; the
+// factors arrive pre-split (hi, lo) from the kernels that produce them.
+//
+// CTA = 8 consumer warps + 1 producer warp. The producer streams tiles of M
+// and S (plus the tile's factor panels) with 16-byte cp.async into padded
+// shared-memory rows (conflict-free fragment reads), completing on the
+// stage's mbarrier (cp.async.mbarrier.arrive.noinc); consumers release
+// stages through a second mbarrier. Vectors are packed into the parity's
+// buffer by the consumer threads.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstring>
+
+#include "k_common.cuh"
+
+namespace acp {
+namespace {
+
+constexpr int kTcNW = 8;  // consumer warps
+
+// ---- P-step geometry: tile = 128 rows (one 16-row block per warp) x 32
+// columns, loaded as 2-D TMA boxes (rows of 128 B, SWIZZLE_128B: the 16-byte
+// chunk c of row i sits at chunk c ^ (i & 7)). Each 8-column MMA block j uses
+// chunks j and j + 4 (columns 4j..4j+3, 16+4j..16+4j+3), which makes every
+// fragment read of the tile and of the factor boxes bank-conflict free.
+constexpr int kPTR = 128, kPBC = 32;
+__host__ __device__ constexpr int p_stage_floats(int r8) { return 2 * kPTR * kPBC + 4 * r8 * kPBC; }
+
+struct TcShared {
+  float* ring;
+  uint64_t* full;
+  uint64_t* empty;
+  int stages;
+  int stage_floats;
+};
+
+__device__ __forceinline__ uint32_t lds_u32(const float* p) { return __float_as_uint(*p); }
+// float offset of (row, 16-byte chunk) in a 128B-swizzled box of 32-float rows
+__device__ __forceinline__ int swz(int row, int chunk) { return row * 32 + ((chunk ^ (row & 7)) << 2); }
+
+// 2-D tensor-map TMA load (box at column c0, row r0) completing on `bar`
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int r0,
+                                            uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(s32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(r0), "r"(s32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void tmap_acquire(const CUtensorMap* map) {
+  asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(
+                   reinterpret_cast<uint64_t>(map))
+               : "memory");
+}
+
+template <int R8>
+__device__ void tcp_producer(const Tables& t, const TcSeg* segs, int sb, int se, const TcShared& sh) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t pol = policy_evict_first();
+  uint64_t pol_keep;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
+  int stage = 0;
+  uint32_t phase = 0;
+  constexpr uint32_t kTx = (uint32_t)(2 * kPTR * kPBC + 4 * R8 * kPBC) * 4u;
+  for (int si = sb; si < se; ++si) {
+    const TcSeg s = segs[si];
+    const LayerDesc& L = t.layers[s.layer];
+    if (!L.mat) continue;
+    const int64_t m = L.m;
+    const float* grad = t.grads[s.layer];
+    const float* S = t.E + L.e_off;
+    const bool v16 = (m % 4 == 0) && ((reinterpret_cast<uintptr_t>(grad) & 15u) == 0);
+    const CUtensorMap* maps = t.tmaps + 8 * (int64_t)s.layer;  // M, S, Q_orth hi/lo, Q_loc hi/lo
+    if (v16 && lane < 6) tmap_acquire(maps + lane);
+    const float* fq[4] = {t.qsplit + L.qs_off, t.qsplit + L.qs_off + (int64_t)R8 * m,
+                          t.qlsplit + L.qs_off, t.qlsplit + L.qs_off + (int64_t)R8 * m};
+    for (int64_t r0 = s.row0; r0 < s.row1; r0 += kPTR) {
+      const int nr = (int)((s.row1 - r0) < kPTR ? (s.row1 - r0) : kPTR);
+      for (int64_t c0 = 0; c0 < m; c0 += kPBC) {
+        if (lane == 0) mbar_wait(&sh.empty[stage], phase ^ 1u);
+        __syncwarp();
+        float* dM = sh.ring + (size_t)stage * sh.stage_floats;
+        float* dS = dM + kPTR * kPBC;
+        float* dF = dS + kPTR * kPBC;
+        if (v16) {
+          // boxes: rows beyond n / columns beyond m are zero-filled by the TMA
+          if (lane == 0) {
+            mbar_arrive_tx(&sh.full[stage], kTx);
+            tma_load_2d(dM, maps + 0, (int)c0, (int)r0, &sh.full[stage], pol);
+            tma_load_2d(dS, maps + 1, (int)c0, (int)r0, &sh.full[stage], pol);
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+              tma_load_2d(dF + a * R8 * kPBC, maps + 2 + a, (int)c0, 0, &sh.full[stage], pol_keep);
+          }
+        } else {
+          // unaligned layer: 4-byte async copies into the same swizzled layout
+          if (lane == 0) mbar_arrive(&sh.full[stage]);
+          for (int it = lane; it < kPTR * kPBC; it += 32) {
+            const int i = it / kPBC, j = it - i * kPBC;
+            const bool ok = i < nr && c0 + j < m;
+            const int64_t off = ok ? (r0 + i) * m + c0 + j : 0;
+            const int d = swz(i, j >> 2) + (j & 3);
+            cp_async4(dM + d, grad + off, ok ? 4u : 0u);
+            cp_async4(dS + d, S + off, ok ? 4u : 0u);
+          }
+          for (int it = lane; it < 4 * R8 * kPBC; it += 32) {
+            const int a = it / (R8 * kPBC), rem = it - a * (R8 * kPBC);
+            const int k = rem / kPBC, j = rem - k * kPBC;
+            const bool ok = c0 + j < m;
+            cp_async4(dF + a * R8 * kPBC + swz(k, j >> 2) + (j & 3), fq[a] + (ok ? k * m + c0 + j : 0),
+                      ok ? 4u : 0u);
+          }
+        }
+        cp_async_arrive(&sh.full[stage]);
+        if (++stage == sh.stages) {
+          stage = 0;
+          phase ^= 1u;
+        }
+      }
+    }
+  }
+}
+
+template <int R8>
+__device__ void tcp_consumer(const Tables& t, const TcSeg* segs, int sb, int se, const TcShared& sh) {
+  constexpr int KB = R8 / 8;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, tq = lane & 3;
+  const int rw = 16 * warp + g;  // this lane's first tile row (second: rw + 8, same swizzle)
+  // loop-invariant fragment offsets (floats) inside a stage's boxes, per
+  // 8-column block j: X / Q_orth pairs at chunk cj, correction column at cg
+  int offX[4], offQ[4], offL0[4], offL1[4], colj[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int cj = tq < 2 ? j : j + 4, oc = 2 * (tq & 1);
+    const int cg = g < 4 ? j : j + 4, og = g & 3;
+    offX[j] = swz(rw, cj) + oc;
+    offQ[j] = swz(g, cj) + oc;               // + 256 * nb (rows 8nb + g)
+    offL0[j] = swz(tq, cg) + og;             // + 256 * kb (rows 8kb + tq)
+    offL1[j] = swz(tq + 4, cg) + og;         // rows 8kb + tq + 4
+    colj[j] = 4 * cj + oc;
+  }
+  int stage = 0;
+  uint32_t phase = 0;
+  for (int si = sb; si < se; ++si) {
+    const TcSeg s = segs[si];
+    const LayerDesc& L = t.layers[s.layer];
+    float* grad = t.grads[s.layer];
+    if (!L.mat) {  // vector: pack into the P-buffer slot
+      float* slot = t.pbuf + L.p_off;
+      for (int64_t i = s.row0 + threadIdx.x; i < s.row1; i += kTcNW * 32) slot[i] = grad[i];
+      continue;
+    }
+    const int64_t m = L.m, n = L.n;
+    const int r = L.r;
+    float* S = t.E + L.e_off;
+    const bool v2 = (m % 2 == 0) && ((reinterpret_cast<uintptr_t>(grad) & 7u) == 0);
+    const float* Ps = t.psplit + L.ps_off;   // P_orth [2][n][R8]
+    float* Pl = t.plsplit + L.ps_off;        // P_loc  [2][n][R8]
+    float* Pw = t.pbuf + L.p_off;            // P slot, k-major [r][n]
+    for (int64_t r0 = s.row0; r0 < s.row1; r0 += kPTR) {
+      const int64_t ra = r0 + rw, rb = ra + 8;
+      const bool oka = ra < s.row1, okb = rb < s.row1;
+      // A fragments of P_orth (rows ra, rb; ranks 8kb + tq, + 4), hi and lo;
+      // rows past the segment are zero, so their x (zero-filled tiles) is 0
+      uint32_t ah[KB][4], al[KB][4];
+#pragma unroll
+      for (int kb = 0; kb < KB; ++kb) {
+        const int k0 = 8 * kb + tq;
+        ah[kb][0] = oka ? __float_as_uint(Ps[ra * R8 + k0]) : 0u;
+        ah[kb][1] = okb ? __float_as_uint(Ps[rb * R8 + k0]) : 0u;
+        ah[kb][2] = oka ? __float_as_uint(Ps[ra * R8 + k0 + 4]) : 0u;
+        ah[kb][3] = okb ? __float_as_uint(Ps[rb * R8 + k0 + 4]) : 0u;
+        al[kb][0] = oka ? __float_as_uint(Ps[(n + ra) * R8 + k0]) : 0u;
+        al[kb][1] = okb ? __float_as_uint(Ps[(n + rb) * R8 + k0]) : 0u;
+        al[kb][2] = oka ? __float_as_uint(Ps[(n + ra) * R8 + k0 + 4]) : 0u;
+        al[kb][3] = okb ? __float_as_uint(Ps[(n + rb) * R8 + k0 + 4]) : 0u;
+      }
+      float acc[KB][4];
+#pragma unroll
+      for (int kb = 0; kb < KB; ++kb) acc[kb][0] = acc[kb][1] = acc[kb][2] = acc[kb][3] = 0.f;
+      const bool rows_full = r0 + kPTR <= s.row1;
+      float* Sa = S + ra * m;
+      float* Sb = S + rb * m;
+      for (int64_t c0 = 0; c0 < m; c0 += kPBC) {
+        mbar_wait(&sh.full[stage], phase);
+        const float* sM = sh.ring + (size_t)stage * sh.stage_floats;
+        const float* sS = sM + kPTR * kPBC;
+        const float* fQh = sS + kPTR * kPBC;
+        const float* fQl = fQh + R8 * kPBC;
+        const float* fLh = fQl + R8 * kPBC;
+        const float* fLl = fLh + R8 * kPBC;
+        const bool full = rows_full && (c0 + kPBC <= m) && v2;
+        // the tensor core accumulates with truncation: keep each MMA chain
+        // short (one panel) and sum the panels in fp32 round-to-nearest
+        float pa[KB][4];
+#pragma unroll
+        for (int kb = 0; kb < KB; ++kb) pa[kb][0] = pa[kb][1] = pa[kb][2] = pa[kb][3] = 0.f;
+#pragma unroll
+        for (int j = 0; j < kPBC / 8; ++j) {
+          // correction C = P_orth Q_loc^T (16 rows x 8 columns)
+          float c[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int kb = 0; kb < KB; ++kb) {
+            const int o0 = offL0[j] + 256 * kb, o1 = offL1[j] + 256 * kb;
+            mma3(c, ah[kb], al[kb], lds_u32(fLh + o0), lds_u32(fLh + o1), lds_u32(fLl + o0),
+                 lds_u32(fLl + o1));
+          }
+          const float2 m0 = *reinterpret_cast<const float2*>(sM + offX[j]);
+          const float2 m1 = *reinterpret_cast<const float2*>(sM + offX[j] + 256);
+          const float2 s0 = *reinterpret_cast<const float2*>(sS + offX[j]);
+          const float2 s1 = *reinterpret_cast<const float2*>(sS + offX[j] + 256);
+          const float x0 = m0.x + s0.x - c[0], x1 = m0.y + s0.y - c[1];
+          const float x2 = m1.x + s1.x - c[2], x3 = m1.y + s1.y - c[3];
+          const int64_t col = c0 + colj[j];
+          if (full) {
+            __stcs(reinterpret_cast<float2*>(Sa + col), make_float2(x0, x1));
+            __stcs(reinterpret_cast<float2*>(Sb + col), make_float2(x2, x3));
+          } else {
+            const bool ca0 = col < m, ca1 = col + 1 < m;
+            if (oka && ca0) Sa[col] = x0;
+            if (oka && ca1) Sa[col + 1] = x1;
+            if (okb && ca0) Sb[col] = x2;
+            if (okb && ca1) Sb[col + 1] = x3;
+          }
+          // projection P += x Q_orth; A's k index t <-> column n = 2t, t + 4 <-> 2t + 1
+          uint32_t xh[4], xl[4];
+          split_tf32(x0, xh[0], xl[0]);
+          split_tf32(x2, xh[1], xl[1]);
+          split_tf32(x1, xh[2], xl[2]);
+          split_tf32(x3, xh[3], xl[3]);
+#pragma unroll
+          for (int nb = 0; nb < KB; ++nb) {
+            const int o = offQ[j] + 256 * nb;
+            const float2 bh = *reinterpret_cast<const float2*>(fQh + o);
+            const float2 bl = *reinterpret_cast<const float2*>(fQl + o);
+            mma3(pa[nb], xh, xl, __float_as_uint(bh.x), __float_as_uint(bh.y),
+                 __float_as_uint(bl.x), __float_as_uint(bl.y));
+          }
+        }
+#pragma unroll
+        for (int kb = 0; kb < KB; ++kb) {
+          acc[kb][0] += pa[kb][0];
+          acc[kb][1] += pa[kb][1];
+          acc[kb][2] += pa[kb][2];
+          acc[kb][3] += pa[kb][3];
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sh.empty[stage]);
+        if (++stage == sh.stages) {
+          stage = 0;
+          phase ^= 1u;
+        }
+      }
+      // P_loc rows -> P slot (k-major, all-reduce payload) + split copy
+#pragma unroll
+      for (int nb = 0; nb < KB; ++nb) {
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const int k = 8 * nb + 2 * tq + (h & 1);
+          const int64_t row = (h < 2) ? ra : rb;
+          const bool ok = (h < 2) ? oka : okb;
+          if (ok && k < r) {
+            const float v = acc[nb][h];
+            Pw[(int64_t)k * n + row] = v;
+            uint32_t hi, lo;
+            split_tf32(v, hi, lo);
+            Pl[row * R8 + k] = __uint_as_float(hi);
+            Pl[(n + row) * R8 + k] = __uint_as_float(lo);
+          }
+        }
+      }
+    }
+  }
+}
+
+// ---- Q-step: tiles of tr rows x pc columns, staged as pc/32 boxes of
+// tr x 32 floats (SWIZZLE_128B); warps own 16-column blocks (cbw each) and
+// walk the tile's 8-row k-steps. Scalar reads (row 2t / 2t+1, column g / g+8)
+// hit 32 distinct banks under the swizzle. Row factors (P_loc, P_orth hi/lo)
+// arrive by cp.async into rows of R8 + 4 floats.
+constexpr int kQRS_PAD = 4;
+
+__host__ __device__ constexpr int q_nbox(int pc) { return (pc + 31) / 32; }
+__host__ __device__ constexpr int q_stage_floats(int tr, int pc, int r8) {
+  return (2 * q_nbox(pc) * tr * 32 + 4 * tr * (r8 + kQRS_PAD) + 255) / 256 * 256;
+}
+
+template <int R8>
+__device__ void tcq_producer(const Tables& t, const TcSeg* segs, int sb, int se, const TcShared& sh) {
+  constexpr int RS = R8 + kQRS_PAD;
+  const int lane = threadIdx.x & 31;
+  const uint64_t pol = policy_evict_first();
+  int stage = 0;
+  uint32_t phase = 0;
+  for (int si = sb; si < se; ++si) {
+    const TcSeg s = segs[si];
+    const LayerDesc& L = t.layers[s.layer];
+    if (!L.mat) continue;
+    const int64_t m = L.m, n = L.n;
+    const TcMap mp = L.tq;
+    const float* grad = t.grads[s.layer];
+    const float* S = t.E + L.e_off;
+    const int64_t c0 = (int64_t)s.panel * mp.pc;
+    const int cols = (int)((m - c0) < mp.pc ? (m - c0) : mp.pc);
+    const int nbox = q_nbox(mp.pc);
+    const int tr = mp.tr;
+    const bool v16 = (m % 4 == 0) && ((reinterpret_cast<uintptr_t>(grad) & 15u) == 0);
+    const CUtensorMap* maps = t.tmaps + 8 * (int64_t)s.layer + 6;  // M, S with tr-row boxes
+    if (v16 && lane < 2) tmap_acquire(maps + lane);
+    const float* fr[4] = {t.plsplit + L.ps_off, t.plsplit + L.ps_off + n * R8,
+                          t.psplit + L.ps_off, t.psplit + L.ps_off + n * R8};
+    for (int64_t r0 = s.row0; r0 < s.row1; r0 += tr) {
+      const int nr = (int)((s.row1 - r0) < tr ? (s.row1 - r0) : tr);
+      if (lane == 0) mbar_wait(&sh.empty[stage], phase ^ 1u);
+      __syncwarp();
+      float* dM = sh.ring + (size_t)stage * sh.stage_floats;
+      float* dS = dM + nbox * tr * 32;
+      float* dF = dS + nbox * tr * 32;
+      if (v16) {
+        if (lane == 0) {
+          mbar_arrive_tx(&sh.full[stage], 2u * (uint32_t)(nbox * tr * 32 * 4));
+          for (int b = 0; b < nbox; ++b) {
+            tma_load_2d(dM + b * tr * 32, maps + 0, (int)(c0 + 32 * b), (int)r0, &sh.full[stage], pol);
+            tma_load_2d(dS + b * tr * 32, maps + 1, (int)(c0 + 32 * b), (int)r0, &sh.full[stage], pol);
+          }
+        }
+      } else {
+        if (lane == 0) mbar_arrive(&sh.full[stage]);
+        for (int it = lane; it < tr * nbox * 32; it += 32) {
+          const int i = it / (nbox * 32), col = it - i * (nbox * 32);
+          const bool ok = i < nr && col < cols;
+          const int64_t off = ok ? (r0 + i) * m + c0 + col : 0;
+          const int w = col & 31;
+          const int d = (col >> 5) * tr * 32 + swz(i, w >> 2) + (w & 3);
+          cp_async4(dM + d, grad + off, ok ? 4u : 0u);
+          cp_async4(dS + d, S + off, ok ? 4u : 0u);
+        }
+      }
+      // row factors [row][R8] (P_loc hi, lo, P_orth hi, lo): 16-byte chunks
+      for (int it = lane; it < 4 * tr * (R8 / 4); it += 32) {
+        const int a = it / (tr * (R8 / 4)), rem = it - a * (tr * (R8 / 4));
+        const int i = rem / (R8 / 4), j = rem - i * (R8 / 4);
+        const bool ok = i < nr;
+        cp_async16(dF + (a * tr + i) * RS + 4 * j, fr[a] + (ok ? (r0 + i) * R8 + 4 * j : 0),
+                   ok ? 16u : 0u);
+      }
+      cp_async_arrive(&sh.full[stage]);
+      if (++stage == sh.stages) {
+        stage = 0;
+        phase ^= 1u;
+      }
+    }
+  }
+}
+
+template <int R8, int CBW>
+__device__ void tcq_consumer(const Tables& t, const TcSeg* segs, int sb, int se, const TcShared& sh) {
+  constexpr int KB = R8 / 8;
+  constexpr int RS = R8 + kQRS_PAD;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, tq = lane & 3;
+  int stage = 0;
+  uint32_t phase = 0;
+  for (int si = sb; si < se; ++si) {
+    const TcSeg s = segs[si];
+    const LayerDesc& L = t.layers[s.layer];
+    float* grad = t.grads[s.layer];
+    if (!L.mat) {  // vector: pack into the Q-buffer slot
+      float* slot = t.qbuf + L.q_off;
+      for (int64_t i = s.row0 + threadIdx.x; i < s.row1; i += kTcNW * 32) slot[i] = grad[i];
+      continue;
+    }
+    const int64_t m = L.m;
+    const int r = L.r;
+    const TcMap mp = L.tq;
+    float* S = t.E + L.e_off;
+    const int64_t c0 = (int64_t)s.panel * mp.pc;
+    const int cols = (int)((m - c0) < mp.pc ? (m - c0) : mp.pc);
+    const int nbox = q_nbox(mp.pc);
+    const int tr = mp.tr;
+    const int cg = warp % mp.wc, rg = warp / mp.wc;
+    const int ksteps = tr / 8;
+    const float* Qh = t.qsplit + L.qs_off;   // Q_orth [2][R8][m]
+    const float* Ql = Qh + (int64_t)R8 * m;
+    // this warp's column blocks (16 columns each) inside the panel
+    uint32_t ah[CBW][KB][4], al[CBW][KB][4];
+    float acc[CBW][KB][4];
+    int offa[CBW], offb[CBW];  // x at (row 2t, column g) and (row 2t, column g + 8); rows 2t+1: + 32 / xor
+    int offa1[CBW], offb1[CBW];
+    bool blk[CBW];
+#pragma unroll
+    for (int j = 0; j < CBW; ++j) {
+      const int cl = (cg * CBW + j) * 16;
+      blk[j] = cl < mp.pc;  // uniform per warp
+      const int64_t ca = c0 + cl + g, cb2 = ca + 8;
+      const bool oka = cl + g < cols, okb = cl + g + 8 < cols;
+#pragma unroll
+      for (int kb = 0; kb < KB; ++kb) {
+        const int64_t k0 = 8 * kb + tq;
+        ah[j][kb][0] = oka ? __float_as_uint(Qh[k0 * m + ca]) : 0u;
+        ah[j][kb][1] = okb ? __float_as_uint(Qh[k0 * m + cb2]) : 0u;
+        ah[j][kb][2] = oka ? __float_as_uint(Qh[(k0 + 4) * m + ca]) : 0u;
+        ah[j][kb][3] = okb ? __float_as_uint(Qh[(k0 + 4) * m + cb2]) : 0u;
+        al[j][kb][0] = oka ? __float_as_uint(Ql[k0 * m + ca]) : 0u;
+        al[j][kb][1] = okb ? __float_as_uint(Ql[k0 * m + cb2]) : 0u;
+        al[j][kb][2] = oka ? __float_as_uint(Ql[(k0 + 4) * m + ca]) : 0u;
+        al[j][kb][3] = okb ? __float_as_uint(Ql[(k0 + 4) * m + cb2]) : 0u;
+        acc[j][kb][0] = acc[j][kb][1] = acc[j][kb][2] = acc[j][kb][3] = 0.f;
+      }
+      const int box = (cl >> 5) * tr * 32, w = (cl & 31) + g;
+      offa[j] = box + swz(2 * tq, w >> 2) + (w & 3);
+      offb[j] = box + swz(2 * tq, (w + 8) >> 2) + (w & 3);
+      offa1[j] = box + swz(2 * tq + 1, w >> 2) + (w & 3);
+      offb1[j] = box + swz(2 * tq + 1, (w + 8) >> 2) + (w & 3);
+    }
+    for (int64_t r0 = s.row0; r0 < s.row1; r0 += tr) {
+      mbar_wait(&sh.full[stage], phase);
+      const float* sM = sh.ring + (size_t)stage * sh.stage_floats;
+      const float* sS = sM + nbox * tr * 32;
+      const float* fLh = sS + nbox * tr * 32;   // P_loc hi [tr][RS]
+      const float* fLl = fLh + tr * RS;
+      const float* fPh = fLl + tr * RS;   // P_orth hi
+      const float* fPl = fPh + tr * RS;
+      const bool full = (r0 + tr <= s.row1) && (mp.pc <= cols);
+      float ta[CBW][KB][4];  // this tile's sums (short MMA chains, see the P-step)
+#pragma unroll
+      for (int j = 0; j < CBW; ++j)
+#pragma unroll
+        for (int kb = 0; kb < KB; ++kb) ta[j][kb][0] = ta[j][kb][1] = ta[j][kb][2] = ta[j][kb][3] = 0.f;
+      for (int ks = rg; ks < ksteps; ks += mp.wr) {
+        const int rowg = 8 * ks + g, rowa = 8 * ks + 2 * tq, rowb = rowa + 1;
+        // B fragments: P_loc (k = rank, n = row) and P_orth (k = row, n = rank)
+        uint32_t lbh[KB][2], lbl[KB][2], pbh[KB][2], pbl[KB][2];
+#pragma unroll
+        for (int kb = 0; kb < KB; ++kb) {
+          lbh[kb][0] = lds_u32(fLh + rowg * RS + 8 * kb + tq);
+          lbh[kb][1] = lds_u32(fLh + rowg * RS + 8 * kb + tq + 4);
+          lbl[kb][0] = lds_u32(fLl + rowg * RS + 8 * kb + tq);
+          lbl[kb][1] = lds_u32(fLl + rowg * RS + 8 * kb + tq + 4);
+          pbh[kb][0] = lds_u32(fPh + rowa * RS + 8 * kb + g);
+          pbh[kb][1] = lds_u32(fPh + rowb * RS + 8 * kb + g);
+          pbl[kb][0] = lds_u32(fPl + rowa * RS + 8 * kb + g);
+          pbl[kb][1] = lds_u32(fPl + rowb * RS + 8 * kb + g);
+        }
+        const int ko = 256 * ks;  // 8 rows = 8 x 32 floats, same swizzle
+        float* Sa = S + (r0 + rowa) * m + c0;
+        float* Sb = Sa + m;
+#pragma unroll
+        for (int j = 0; j < CBW; ++j) {
+          if (!blk[j]) continue;
+          // correction C^T = Q_orth P_loc^T (16 columns x 8 rows)
+          float c[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int kb = 0; kb < KB; ++kb)
+            mma3(c, ah[j][kb], al[j][kb], lbh[kb][0], lbh[kb][1], lbl[kb][0], lbl[kb][1]);
+          // c0 (col g, row 2t), c1 (col g, row 2t+1), c2 (col g+8, row 2t), c3 (col g+8, row 2t+1)
+          const float x0 = sM[offa[j] + ko] + sS[offa[j] + ko] - c[0];
+          const float x1 = sM[offa1[j] + ko] + sS[offa1[j] + ko] - c[1];
+          const float x2 = sM[offb[j] + ko] + sS[offb[j] + ko] - c[2];
+          const float x3 = sM[offb1[j] + ko] + sS[offb1[j] + ko] - c[3];
+          const int ca = (cg * CBW + j) * 16 + g, cb2 = ca + 8;
+          if (full) {
+            __stcs(Sa + ca, x0);
+            __stcs(Sb + ca, x1);
+            __stcs(Sa + cb2, x2);
+            __stcs(Sb + cb2, x3);
+          } else {
+            const bool va = r0 + rowa < s.row1, vb = r0 + rowb < s.row1;
+            if (ca < cols) {
+              if (va) __stcs(Sa + ca, x0);
+              if (vb) __stcs(Sb + ca, x1);
+            }
+            if (cb2 < cols) {
+              if (va) __stcs(Sa + cb2, x2);
+              if (vb) __stcs(Sb + cb2, x3);
+            }
+          }
+          // projection Q += x^T P_orth: A = x^T (columns x rows), k t <-> row 2t
+          uint32_t xh[4], xl[4];
+          split_tf32(x0, xh[0], xl[0]);
+          split_tf32(x2, xh[1], xl[1]);
+          split_tf32(x1, xh[2], xl[2]);
+          split_tf32(x3, xh[3], xl[3]);
+#pragma unroll
+          for (int nb = 0; nb < KB; ++nb)
+            mma3(ta[j][nb], xh, xl, pbh[nb][0], pbh[nb][1], pbl[nb][0], pbl[nb][1]);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < CBW; ++j)
+#pragma unroll
+        for (int kb = 0; kb < KB; ++kb) {
+          acc[j][kb][0] += ta[j][kb][0];
+          acc[j][kb][1] += ta[j][kb][1];
+          acc[j][kb][2] += ta[j][kb][2];
+          acc[j][kb][3] += ta[j][kb][3];
+        }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sh.empty[stage]);
+      if (++stage == sh.stages) {
+        stage = 0;
+        phase ^= 1u;
+      }
+    }
+    // partial slot of row group rg: k-major [r][pc]
+    const int64_t stride = ((int64_t)r * mp.pc + 3) / 4 * 4;
+    float* part = t.colpart + s.part_off + rg * stride;
+#pragma unroll
+    for (int j = 0; j < CBW; ++j) {
+      const int cl = (cg * CBW + j) * 16;
+      if (cl >= cols) break;
+#pragma unroll
+      for (int nb = 0; nb < KB; ++nb) {
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const int k = 8 * nb + 2 * tq + (h & 1);
+          const int col = cl + g + ((h & 2) ? 8 : 0);
+          if (k < r && col < cols) part[(int64_t)k * mp.pc + col] = acc[j][nb][h];
+        }
+      }
+    }
+  }
+}
+
+template <int MODE, int R8>
+__global__ void __launch_bounds__(kTcNW * 32 + 32, 1)
+tc_kernel(Tables t, const TcSeg* __restrict__ segs, const int32_t* __restrict__ cta_begin,
+          int stages, int stage_floats) {
+  extern __shared__ __align__(1024) unsigned char tc_smem_raw[];  // SWIZZLE_128B boxes
+  TcShared sh;
+  sh.stages = stages;
+  sh.stage_floats = stage_floats;
+  // 1024-byte aligned ring (the launch reserves the slack)
+  sh.ring = reinterpret_cast<float*>(tc_smem_raw + ((1024u - (s32(tc_smem_raw) & 1023u)) & 1023u));
+  sh.full = reinterpret_cast<uint64_t*>(sh.ring + (size_t)stages * stage_floats);
+  sh.empty = sh.full + stages;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < stages; ++i) {
+      mbar_init(&sh.full[i], 33);      // lane 0's expect-tx arrive + one noinc arrive per lane
+      mbar_init(&sh.empty[i], kTcNW);  // one arrive per consumer warp
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int sb = cta_begin[blockIdx.x], se = cta_begin[blockIdx.x + 1];
+  const bool producer = (threadIdx.x >> 5) == kTcNW;
+  if constexpr (MODE == 0) {
+    if (producer) tcp_producer<R8>(t, segs, sb, se, sh);
+    else tcp_consumer<R8>(t, segs, sb, se, sh);
+  } else {
+    if (producer) tcq_producer<R8>(t, segs, sb, se, sh);
+    else tcq_consumer<R8, (R8 <= 16 ? 2 : 1)>(t, segs, sb, se, sh);
+  }
+}
+
+// TC state -> E (eager, rare): dst = S - A B^T with A [2][n][R8], B [2][R8][m]
+__global__ void tc_materialize_kernel(Tables t, LayerDesc L, int which, float* dst) {
+  const int64_t n = L.n, m = L.m;
+  const int r = L.r, R8 = t.r8;
+  const float* S = t.E + L.e_off;
+  const float* A = (which == 1 ? t.psplit : t.plsplit) + L.ps_off;
+  const float* B = (which == 1 ? t.qlsplit : t.qsplit) + L.qs_off;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n * m;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = idx / m, j = idx - i * m;
+    float x = S[idx];
+    for (int k = 0; k < r; ++k) {
+      const float a = A[i * R8 + k] + A[(n + i) * R8 + k];
+      const float b = B[(int64_t)k * m + j] + B[((int64_t)R8 + k) * m + j];
+      x = fmaf(-a, b, x);
+    }
+    dst[idx] = x;
+  }
+}
+
+}  // namespace
+
+int tc_p_stage_floats(int r8) { return p_stage_floats(r8); }
+
+int tc_q_map(int64_t m, int r8, TcMap* out) {
+  const int cbw = r8 <= 16 ? 2 : 1;
+  const int64_t maxpc = (int64_t)16 * cbw * kTcNW;
+  const int64_t np = (m + maxpc - 1) / maxpc;
+  int64_t pc = (m + np - 1) / np;
+  pc = (pc + 15) / 16 * 16;
+  const int ncb = (int)(pc / 16);
+  const int need = (ncb + cbw - 1) / cbw;
+  int wc = 1;
+  while (wc < need && wc < kTcNW) wc <<= 1;
+  const int wr = kTcNW / wc;
+  const int tr = 8 * (wr > 2 ? wr : 2);
+  out->pc = (int32_t)pc;
+  out->np = (int16_t)np;
+  out->wc = (int16_t)wc;
+  out->wr = (int16_t)wr;
+  out->tr = (int16_t)tr;
+  out->cbw = (int16_t)cbw;
+  out->pad_ = 0;
+  return q_stage_floats(tr, (int)pc, r8);
+}
+
+size_t tc_smem_bytes(int stages, int stage_floats) {
+  return (size_t)stages * stage_floats * 4 + (size_t)stages * 16 + 1024;
+}
+
+// Host: 2-D fp32 tensor map (inner dim `cols`, `rows` rows, row pitch `cols`
+// floats) with a box of 32 columns x box_rows rows, SWIZZLE_128B, zero OOB fill.
+static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+bool tc_encode_map(CUtensorMap* out, const float* base, int64_t cols, int64_t rows, int box_rows) {
+  std::memset(out, 0, sizeof(CUtensorMap));
+  auto enc = tmap_encoder();
+  if (!enc || !base || cols % 4 != 0 || (reinterpret_cast<uintptr_t>(base) & 15u) != 0) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)cols * 4};
+  const cuuint32_t box[2] = {(cuuint32_t)kPBC, (cuuint32_t)box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+int tc_p_box_rows() { return kPTR; }
+
+cudaError_t launch_tc(int mode, int r8, const Tables& t, const TcSeg* segs, const int32_t* cb, int ncta,
+                      int stages, int stage_floats, cudaStream_t st) {
+  if (ncta <= 0) return cudaSuccess;
+  const size_t smem = tc_smem_bytes(stages, stage_floats);
+  auto go = [&](auto kern) -> cudaError_t {
+    cudaError_t e = allow_max_smem(reinterpret_cast<const void*>(kern));
+    if (e != cudaSuccess) return e;
+    kern<<<ncta, kTcNW * 32 + 32, smem, st>>>(t, segs, cb, stages, stage_floats);
+    return cudaGetLastError();
+  };
+  switch (mode * 100 + r8) {
+    case 8: return go(tc_kernel<0, 8>);
+    case 16: return go(tc_kernel<0, 16>);
+    case 32: return go(tc_kernel<0, 32>);
+    case 108: return go(tc_kernel<1, 8>);
+    case 116: return go(tc_kernel<1, 16>);
+    case 132: return go(tc_kernel<1, 32>);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_tc_materialize(const Tables& t, const LayerDesc& L, int which, float* dst,
+                                  cudaStream_t s) {
+  if (!L.mat) return cudaSuccess;
+  const int64_t total = L.n * L.m;
+  const int grid = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+  tc_materialize_kernel<<<grid, 256, 0, s>>>(t, L, which, dst ? dst : t.E + L.e_off);
+  return cudaGetLastError();
+}
+
+}  // namespace acp

@@ -131,13 +131,17 @@ def test_pack_unpack_bit_exact_and_state_roundtrip():
     ctx2.set_state(1, P, Q, E)
     P2, Q2, E2 = ctx2.get_state(1)
     assert torch.equal(P, P2) and torch.equal(Q, Q2) and torch.equal(E, E2)
-    # resume: both contexts now produce identical next steps
+    # resume: both contexts now produce the same next step. The running
+    # context still holds the residual implicitly (E = S - P_loc Q^T, applied
+    # inside the next projection) while the restored one starts
+    # from the materialised E, so the two agree to fp32 rounding, not bitwise.
     h1 = [torch.randn(s, device="cuda", generator=torch.Generator("cuda").manual_seed(5)) for s in shapes]
     h2 = [x.clone() for x in h1]
     ctx.step(h1, 1)
     ctx2.step(h2, 1)
     for a, b in zip(h1, h2):
-        assert torch.equal(a, b)
+        err = (torch.linalg.vector_norm(a - b) / torch.linalg.vector_norm(b)).item()
+        assert err <= 1e-6, err
     ctx.close()
     ctx2.close()
 

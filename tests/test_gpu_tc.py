@@ -1,0 +1,69 @@
+"""GPU parity of the tensor-core K1 path (k_tc.cu: mma.sync TF32 in 3xTF32
+form, double-deferred residual). It is the default for r >= 8;
+ACP_TC=1 forces it at lower ranks so every rank class is covered here.
+Tolerance as everywhere: relative Frobenius <= 1e-4 per tensor per step."""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import cuda_available
+from acp_harness import make_inputs, make_q0, run_gpu_simulated, run_oracle, compare
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not cuda_available(), reason="needs a CUDA GPU")]
+
+SEED = 2306088
+RAGGED = [(1000,), (64, 3, 7, 7), (2, 1024), (1, 8), (3, 9000), (64, 64), (256, 64), (5, 3, 2),
+          (300, 1152), (17,), (130, 20), (512, 4608), (4, 4), (1000, 1024)]
+
+
+@pytest.fixture
+def force_tc(monkeypatch):
+    monkeypatch.setenv("ACP_TC", "1")
+
+
+@pytest.mark.parametrize("rank", [1, 4])
+def test_tc_forced_low_rank(force_tc, rank):
+    inputs = make_inputs(RAGGED, 2, 6, SEED, "lowrank")
+    q0 = make_q0(RAGGED, rank, SEED)
+    gpu = run_gpu_simulated(RAGGED, rank, inputs, q0=q0, seed=SEED)
+    ref = run_oracle(RAGGED, rank, inputs, q0=q0, seed=SEED)
+    print("worst", compare(RAGGED, gpu, ref, inputs))
+
+
+@pytest.mark.parametrize("parities", [[0, 0, 1, 1, 0, 1], [1, 1, 0, 0, 1]])
+def test_tc_irregular_parities(parities):
+    """Repeated P- or Q-steps force the host to fold the implicit residual into
+    S (tc_materialize_all) before the next projection."""
+    shapes = [(96, 80), (80,), (33, 257), (300, 1152)]
+    inputs = make_inputs(shapes, 2, len(parities), SEED, "gaussian")
+    q0 = make_q0(shapes, 8, SEED)
+    gpu = run_gpu_simulated(shapes, 8, inputs, q0=q0, seed=SEED, parities=parities)
+    ref = run_oracle(shapes, 8, inputs, q0=q0, seed=SEED, parities=parities)
+    compare(shapes, gpu, ref, inputs)
+
+
+def test_tc_graph_replay_and_determinism():
+    import torch
+    from paper_2306_08881_b200 import AcpContext
+    shapes = [(1024, 1024), (64, 3, 3, 3), (4096,), (512, 4608)]
+    outs = []
+    for graphs in (True, False, True):
+        ctx = AcpContext(shapes, 16, seed=3)
+        ctx.set_graphs(graphs)
+        gen = torch.Generator(device="cuda").manual_seed(11)
+        res = []
+        for t in range(4):
+            g = [torch.randn(s, device="cuda", generator=gen) for s in shapes]
+            ctx.step(g, t % 2)
+            res.append([x.clone() for x in g])
+        torch.cuda.synchronize()
+        outs.append(res)
+        ctx.close()
+    for a, b in zip(outs[0], outs[1]):
+        for x, y in zip(a, b):
+            assert torch.equal(x, y)
+    for a, b in zip(outs[0], outs[2]):
+        for x, y in zip(a, b):
+            assert torch.equal(x, y)
