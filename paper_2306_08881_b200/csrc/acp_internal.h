@@ -161,7 +161,7 @@ struct Tables {
   float* plsplit;        // P_loc   [2][n][R8] (written by the P-step TC kernel)
   int32_t r8;            // padded rank (multiple of 8), 0: TC path off
   const CUtensorMap* tmaps;  // TC path: per layer [M, S, Q_orth hi, lo, Q_loc hi, lo] (P-step
-                             // boxes) + [M, S] (Q-step boxes of tq.tr rows): 8 2-D TMA maps
+                             // boxes), [M, S] (Q-step boxes of tq.tr rows), [Q slot]: 9 maps
 };
 
 // launches (all on `stream`, 256 threads, grid = ncta)
@@ -197,8 +197,11 @@ bool stream_make_map(int mode, int64_t m, int rt, StreamMap* out);
 // Tensor-core K1 (k_tc.cu). mode 0: P-step (x = M + S - P_orth Q_loc^T,
 // S = x, P_loc = x Q_orth -> P slot + P_loc split), mode 1: Q-step
 // (x = M + S - P_loc Q_orth^T, S = x, Q partials = x^T P_orth -> colpart).
+// mode 2 / 3: decode on the tensor cores, grad = scale * P Q^T (P-step: the
+// all-reduced P slot with Q_orth; Q-step: P_orth with the all-reduced Q slot).
 cudaError_t launch_tc(int mode, int r8, const Tables& t, const TcSeg* segs, const int32_t* cta_begin,
-                      int ncta, int stages, int stage_floats, cudaStream_t stream);
+                      int ncta, int stages, int stage_floats, float scale, cudaStream_t stream);
+int tc_d_stage_floats(int r8);
 size_t tc_smem_bytes(int stages, int stage_floats);
 // host: encode a 2-D TMA map (fp32 rows x cols, 32-column boxes of box_rows
 // rows, SWIZZLE_128B); false (map zeroed) when the layout does not allow it

@@ -120,7 +120,9 @@ int split_units(const std::vector<Unit>& units, double min_share, int max_grid,
       const double budget = share * (cta + 1) - done;
       int64_t take = (int64_t)std::ceil(budget / u.cost);
       take = (take + u.align - 1) / u.align * u.align;
-      if (take < 1) take = 1;
+      // segment boundaries stay on multiples of align (TC tiles must not
+      // straddle two segments): never less than one aligned chunk
+      if (take < u.align) take = u.align;
       take = std::min(take, u.count - pos);
       emit(u, pos, pos + take);
       ++nseg;
@@ -505,6 +507,11 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
         bytes += 8.0 * L.n;
         continue;
       }
+      if (mode >= 2) {  // decode: grad written (+ the two factors once)
+        bytes += 4.0 * (double)L.n * (double)L.m + 4.0 * L.r * (double)(L.n + L.m);
+        units.push_back({i, -1, L.n, 4.0 * (double)L.m, 128});
+        continue;
+      }
       // algorithmic bytes: M, S read, S written + the factors once
       bytes += 12.0 * (double)L.n * (double)L.m + 4.0 * L.r * (2.0 * L.n + 2.0 * L.m);
       if (mode == 0) {
@@ -521,8 +528,10 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
     ln.mode = mode;
     ln.seg_off = (int64_t)P.tcsegs.size();
     ln.cb_off = (int64_t)P.ctab.size();
-    ln.stage_floats = std::max(4, mode == 0 ? tc_p_stage_floats(P.R8) : tc_q_stage);
-    ln.stages = (int)std::max<int64_t>(2, std::min<int64_t>(6, (200 * 1024) / (4LL * ln.stage_floats)));
+    ln.stage_floats = std::max(4, mode == 0 ? tc_p_stage_floats(P.R8)
+                                            : (mode == 1 ? tc_q_stage : tc_d_stage_floats(P.R8)));
+    ln.stages = (int)std::max<int64_t>(2, std::min<int64_t>(mode >= 2 ? 8 : 6,
+                                                            (200 * 1024) / (4LL * ln.stage_floats)));
     if (tc_smem_bytes(ln.stages, ln.stage_floats) > 227 * 1024) smem_overflow = true;
     int64_t part = 0;
     int prev_layer = -1, prev_panel = -1;
@@ -576,7 +585,7 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
   };
   auto k3_launch = [&](int parity, const std::vector<int>& ts) {
     if (P.psgd && parity == 0) return Launch{};  // Power-SGD decodes once, after Q
-    if (P.tc) return row_launch(parity == 0 ? 1 : 3, ts);  // write-only decodes
+    if (P.tc) return tc_launch(parity == 0 ? 2 : 3, ts);  // write-only decodes
     if (parity == 1 && P.defer) return row_launch(3, ts);  // decode only
     if (parity == 1 && use_stream) return stream_launch(2, ts);
     return row_launch(parity == 0 ? 1 : 2, ts);
@@ -675,7 +684,7 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
   P.off_psplit = take(4 * (size_t)P.ps_elems);
   P.off_plsplit = take(4 * (size_t)P.ps_elems);
   P.off_tcsegs = take(sizeof(TcSeg) * P.tcsegs.size());
-  P.off_tmaps = take(P.tc ? sizeof(CUtensorMap) * 8 * (size_t)P.T : 0);
+  P.off_tmaps = take(P.tc ? sizeof(CUtensorMap) * 9 * (size_t)P.T : 0);
   P.off_step = take(8);
   P.off_defer = take(8);
   P.off_red = take(sizeof(ColReduceTask) * P.redtasks.size());
@@ -788,7 +797,7 @@ acp_status run_k1(acp_ctx* c, int parity, const Launch& ln, cudaStream_t s) {
   cudaError_t e;
   if (ln.kind == 3) {
     e = launch_tc(ln.mode, c->P.R8, c->tab, dev_tcsegs(c, ln), dev_ctab(c, ln), ln.ncta, ln.stages,
-                  ln.stage_floats, s);
+                  ln.stage_floats, 1.0f, s);
     if (e == cudaSuccess && ln.mode == 1 && ln.nred > 0) {
       e = launch_col_reduce(c->tab,
                             reinterpret_cast<const ColReduceTask*>(c->ws + c->P.off_red) + ln.red_off,
@@ -820,7 +829,10 @@ acp_status run_k3(acp_ctx* c, int parity, const Launch& ln, cudaStream_t s) {
   const int ef = c->P.ef ? 1 : 0;
   ProfRec* r = prof_begin(c, parity == 0 ? ACP_K_DECODE_P : ACP_K_DECODE_Q, ln.bytes, s);
   cudaError_t e =
-      ln.kind == 2
+      ln.kind == 3
+          ? launch_tc(ln.mode, c->P.R8, c->tab, dev_tcsegs(c, ln), dev_ctab(c, ln), ln.ncta, ln.stages,
+                      ln.stage_floats, decode_scale(c), s)
+      : ln.kind == 2
           ? launch_stream(ln.mode, c->P.RT, c->tab, dev_streamsegs(c, ln), dev_ctab(c, ln), ln.ncta,
                           decode_scale(c), ln.stages, ln.stage_floats, ln.factor_floats, ln.defer,
                           ln.ptile, s)
@@ -865,12 +877,12 @@ acp_status set_grads(acp_ctx* c, float* const* grads, cudaStream_t s) {
   if (c->P.tc) {
     // TC P-step: TMA maps of the gradients (M) next to the fixed ones (S, factors)
     const Plan& P = c->P;
-    c->tmaps.resize(8 * (size_t)P.T);
+    c->tmaps.resize(9 * (size_t)P.T);
     for (int i = 0; i < P.T; ++i) {
       const LayerDesc& L = P.L[i];
-      CUtensorMap* mp = c->tmaps.data() + 8 * (size_t)i;
+      CUtensorMap* mp = c->tmaps.data() + 9 * (size_t)i;
       if (!L.mat) {
-        std::memset(mp, 0, 8 * sizeof(CUtensorMap));
+        std::memset(mp, 0, 9 * sizeof(CUtensorMap));
         continue;
       }
       const int br = tc_p_box_rows();
@@ -882,6 +894,7 @@ acp_status set_grads(acp_ctx* c, float* const* grads, cudaStream_t s) {
       tc_encode_map(mp + 5, c->tab.qlsplit + L.qs_off + (int64_t)P.R8 * L.m, L.m, P.R8, P.R8);
       tc_encode_map(mp + 6, c->grads_cache[i], L.m, L.n, L.tq.tr);
       tc_encode_map(mp + 7, c->tab.E + L.e_off, L.m, L.n, L.tq.tr);
+      tc_encode_map(mp + 8, c->tab.qbuf + L.q_off, L.m, L.r, P.R8);
     }
     CK(c, cudaMemcpyAsync(c->ws + P.off_tmaps, c->tmaps.data(), sizeof(CUtensorMap) * c->tmaps.size(),
                           cudaMemcpyHostToDevice, s), "tensor map upload");

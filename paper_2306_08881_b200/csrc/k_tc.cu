@@ -42,7 +42,9 @@ constexpr int kTcNW = 8;  // consumer warps
 // chunks j and j + 4 (columns 4j..4j+3, 16+4j..16+4j+3), which makes every
 // fragment read of the tile and of the factor boxes bank-conflict free.
 constexpr int kPTR = 128, kPBC = 32;
-__host__ __device__ constexpr int p_stage_floats(int r8) { return 2 * kPTR * kPBC + 4 * r8 * kPBC; }
+constexpr int kPNB = 2;   // boxes per P-step tile (tile = 128 rows x 64 columns: 256 B per row)
+constexpr int kPBOX = kPTR * kPBC;
+__host__ __device__ constexpr int p_stage_floats(int r8) { return kPNB * (2 * kPBOX + 4 * r8 * kPBC); }
 
 struct TcShared {
   float* ring;
@@ -71,6 +73,73 @@ __device__ __forceinline__ void tmap_acquire(const CUtensorMap* map) {
                : "memory");
 }
 
+// 2-D tensor-map TMA store of a shared-memory box (bulk group; the caller
+// commits and waits for the shared-memory read before reusing the buffer)
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int r0) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(r0), "r"(s32(src))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
+// Stage release with S written back by TMA: thread 0 of the consumers
+// releases a stage only after the store that reads it has read it; the
+// previous tile's stage is released one tile late so the store overlaps.
+struct StageRelease {
+  int pending = -1;
+  __device__ __forceinline__ void after_store(const TcShared& sh, int stage) {
+    bulk_commit();
+    bulk_wait_read<1>();
+    if (pending >= 0) mbar_arrive(&sh.empty[pending]);
+    pending = stage;
+  }
+  __device__ __forceinline__ void immediate(const TcShared& sh, int stage) {
+    if (pending >= 0) {
+      bulk_wait_read<0>();
+      mbar_arrive(&sh.empty[pending]);
+      pending = -1;
+    }
+    mbar_arrive(&sh.empty[stage]);
+  }
+  __device__ __forceinline__ void finish() { bulk_wait_all(); }
+};
+
+// Two adjacent 8-column MMA blocks (jp, jp + 1) of C fragments -> 16-byte
+// stores that fill whole 32-byte sectors: lanes t and t ^ 1 trade one pair so
+// each lane holds 4 consecutive columns of a row (block jp for even t,
+// block jp + 1 for odd t). ca / cb: this lane's own pair columns in the blocks.
+__device__ __forceinline__ void store_pair(float* Ra, float* Rb, int64_t ca, int64_t cb, bool odd,
+                                           const float (&a)[4], const float (&b)[4]) {
+  const float s0 = odd ? a[0] : b[0], s1 = odd ? a[1] : b[1];
+  const float s2 = odd ? a[2] : b[2], s3 = odd ? a[3] : b[3];
+  const float r0 = __shfl_xor_sync(0xffffffffu, s0, 1), r1 = __shfl_xor_sync(0xffffffffu, s1, 1);
+  const float r2 = __shfl_xor_sync(0xffffffffu, s2, 1), r3 = __shfl_xor_sync(0xffffffffu, s3, 1);
+  const int64_t c = odd ? cb - 2 : ca;
+  const float4 va = odd ? make_float4(r0, r1, b[0], b[1]) : make_float4(a[0], a[1], r0, r1);
+  const float4 vb = odd ? make_float4(r2, r3, b[2], b[3]) : make_float4(a[2], a[3], r2, r3);
+  __stcs(reinterpret_cast<float4*>(Ra + c), va);
+  __stcs(reinterpret_cast<float4*>(Rb + c), vb);
+}
+// masked fallback: each lane stores its own pairs (rows / columns checked)
+__device__ __forceinline__ void store_own(float* Ra, float* Rb, int64_t col, int64_t m, bool oka, bool okb,
+                                          const float (&x)[4]) {
+  const bool ca0 = col < m, ca1 = col + 1 < m;
+  if (oka && ca0) Ra[col] = x[0];
+  if (oka && ca1) Ra[col + 1] = x[1];
+  if (okb && ca0) Rb[col] = x[2];
+  if (okb && ca1) Rb[col + 1] = x[3];
+}
+
 template <int R8>
 __device__ void tcp_producer(const Tables& t, const TcSeg* segs, int sb, int se, const TcShared& sh) {
   const int lane = threadIdx.x & 31;
@@ -79,7 +148,7 @@ __device__ void tcp_producer(const Tables& t, const TcSeg* segs, int sb, int se,
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
   int stage = 0;
   uint32_t phase = 0;
-  constexpr uint32_t kTx = (uint32_t)(2 * kPTR * kPBC + 4 * R8 * kPBC) * 4u;
+  constexpr uint32_t kTx = (uint32_t)(kPNB * (2 * kPBOX + 4 * R8 * kPBC)) * 4u;
   for (int si = sb; si < se; ++si) {
     const TcSeg s = segs[si];
     const LayerDesc& L = t.layers[s.layer];
@@ -88,45 +157,50 @@ __device__ void tcp_producer(const Tables& t, const TcSeg* segs, int sb, int se,
     const float* grad = t.grads[s.layer];
     const float* S = t.E + L.e_off;
     const bool v16 = (m % 4 == 0) && ((reinterpret_cast<uintptr_t>(grad) & 15u) == 0);
-    const CUtensorMap* maps = t.tmaps + 8 * (int64_t)s.layer;  // M, S, Q_orth hi/lo, Q_loc hi/lo
+    const CUtensorMap* maps = t.tmaps + 9 * (int64_t)s.layer;  // M, S, Q_orth hi/lo, Q_loc hi/lo
     if (v16 && lane < 6) tmap_acquire(maps + lane);
     const float* fq[4] = {t.qsplit + L.qs_off, t.qsplit + L.qs_off + (int64_t)R8 * m,
                           t.qlsplit + L.qs_off, t.qlsplit + L.qs_off + (int64_t)R8 * m};
     for (int64_t r0 = s.row0; r0 < s.row1; r0 += kPTR) {
       const int nr = (int)((s.row1 - r0) < kPTR ? (s.row1 - r0) : kPTR);
-      for (int64_t c0 = 0; c0 < m; c0 += kPBC) {
+      for (int64_t c0 = 0; c0 < m; c0 += kPNB * kPBC) {
         if (lane == 0) mbar_wait(&sh.empty[stage], phase ^ 1u);
         __syncwarp();
+        // stage: [M box b][S box b][factor a, box b] (a: Q_orth hi, lo, Q_loc hi, lo)
         float* dM = sh.ring + (size_t)stage * sh.stage_floats;
-        float* dS = dM + kPTR * kPBC;
-        float* dF = dS + kPTR * kPBC;
+        float* dS = dM + kPNB * kPBOX;
+        float* dF = dS + kPNB * kPBOX;
         if (v16) {
           // boxes: rows beyond n / columns beyond m are zero-filled by the TMA
           if (lane == 0) {
             mbar_arrive_tx(&sh.full[stage], kTx);
-            tma_load_2d(dM, maps + 0, (int)c0, (int)r0, &sh.full[stage], pol);
-            tma_load_2d(dS, maps + 1, (int)c0, (int)r0, &sh.full[stage], pol);
 #pragma unroll
-            for (int a = 0; a < 4; ++a)
-              tma_load_2d(dF + a * R8 * kPBC, maps + 2 + a, (int)c0, 0, &sh.full[stage], pol_keep);
+            for (int b = 0; b < kPNB; ++b) {
+              const int cb = (int)c0 + kPBC * b;
+              tma_load_2d(dM + b * kPBOX, maps + 0, cb, (int)r0, &sh.full[stage], pol);
+              tma_load_2d(dS + b * kPBOX, maps + 1, cb, (int)r0, &sh.full[stage], pol);
+#pragma unroll
+              for (int a = 0; a < 4; ++a)
+                tma_load_2d(dF + (a * kPNB + b) * R8 * kPBC, maps + 2 + a, cb, 0, &sh.full[stage], pol_keep);
+            }
           }
         } else {
           // unaligned layer: 4-byte async copies into the same swizzled layout
           if (lane == 0) mbar_arrive(&sh.full[stage]);
-          for (int it = lane; it < kPTR * kPBC; it += 32) {
-            const int i = it / kPBC, j = it - i * kPBC;
+          for (int it = lane; it < kPTR * kPNB * kPBC; it += 32) {
+            const int i = it / (kPNB * kPBC), j = it - i * (kPNB * kPBC);
             const bool ok = i < nr && c0 + j < m;
             const int64_t off = ok ? (r0 + i) * m + c0 + j : 0;
-            const int d = swz(i, j >> 2) + (j & 3);
+            const int d = (j >> 5) * kPBOX + swz(i, (j & 31) >> 2) + (j & 3);
             cp_async4(dM + d, grad + off, ok ? 4u : 0u);
             cp_async4(dS + d, S + off, ok ? 4u : 0u);
           }
-          for (int it = lane; it < 4 * R8 * kPBC; it += 32) {
-            const int a = it / (R8 * kPBC), rem = it - a * (R8 * kPBC);
-            const int k = rem / kPBC, j = rem - k * kPBC;
+          for (int it = lane; it < 4 * R8 * kPNB * kPBC; it += 32) {
+            const int a = it / (R8 * kPNB * kPBC), rem = it - a * (R8 * kPNB * kPBC);
+            const int k = rem / (kPNB * kPBC), j = rem - k * (kPNB * kPBC);
             const bool ok = c0 + j < m;
-            cp_async4(dF + a * R8 * kPBC + swz(k, j >> 2) + (j & 3), fq[a] + (ok ? k * m + c0 + j : 0),
-                      ok ? 4u : 0u);
+            cp_async4(dF + (a * kPNB + (j >> 5)) * R8 * kPBC + swz(k, (j & 31) >> 2) + (j & 3),
+                      fq[a] + (ok ? k * m + c0 + j : 0), ok ? 4u : 0u);
           }
         }
         cp_async_arrive(&sh.full[stage]);
@@ -172,7 +246,10 @@ __device__ void tcp_consumer(const Tables& t, const TcSeg* segs, int sb, int se,
     const int64_t m = L.m, n = L.n;
     const int r = L.r;
     float* S = t.E + L.e_off;
-    const bool v2 = (m % 2 == 0) && ((reinterpret_cast<uintptr_t>(grad) & 7u) == 0);
+    // S: 16-byte stores of whole 32-byte sectors (lane pairs trade a column
+    // pair); a shared-memory + TMA store variant needs a CTA barrier per tile
+    // and measured slower here (1.10 vs 0.83 ms, BERT-L r = 8)
+    const bool v4 = (m % 4 == 0) && ((reinterpret_cast<uintptr_t>(grad) & 15u) == 0);
     const float* Ps = t.psplit + L.ps_off;   // P_orth [2][n][R8]
     float* Pl = t.plsplit + L.ps_off;        // P_loc  [2][n][R8]
     float* Pw = t.pbuf + L.p_off;            // P slot, k-major [r][n]
@@ -200,61 +277,74 @@ __device__ void tcp_consumer(const Tables& t, const TcSeg* segs, int sb, int se,
       const bool rows_full = r0 + kPTR <= s.row1;
       float* Sa = S + ra * m;
       float* Sb = S + rb * m;
-      for (int64_t c0 = 0; c0 < m; c0 += kPBC) {
+      for (int64_t c00 = 0; c00 < m; c00 += kPNB * kPBC) {
         mbar_wait(&sh.full[stage], phase);
-        const float* sM = sh.ring + (size_t)stage * sh.stage_floats;
-        const float* sS = sM + kPTR * kPBC;
-        const float* fQh = sS + kPTR * kPBC;
-        const float* fQl = fQh + R8 * kPBC;
-        const float* fLh = fQl + R8 * kPBC;
-        const float* fLl = fLh + R8 * kPBC;
-        const bool full = rows_full && (c0 + kPBC <= m) && v2;
+        const float* sM0 = sh.ring + (size_t)stage * sh.stage_floats;
+        const float* sS0 = sM0 + kPNB * kPBOX;
+        const float* fF0 = sS0 + kPNB * kPBOX;
+        const bool full = rows_full && (c00 + kPNB * kPBC <= m) && v4;
         // the tensor core accumulates with truncation: keep each MMA chain
         // short (one panel) and sum the panels in fp32 round-to-nearest
         float pa[KB][4];
 #pragma unroll
         for (int kb = 0; kb < KB; ++kb) pa[kb][0] = pa[kb][1] = pa[kb][2] = pa[kb][3] = 0.f;
 #pragma unroll
-        for (int j = 0; j < kPBC / 8; ++j) {
-          // correction C = P_orth Q_loc^T (16 rows x 8 columns)
-          float c[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int bx = 0; bx < kPNB; ++bx) {
+        const int64_t c0 = c00 + kPBC * bx;
+        const float* sM = sM0 + bx * kPBOX;
+        const float* sS = sS0 + bx * kPBOX;
+        const float* fQh = fF0 + (0 * kPNB + bx) * R8 * kPBC;
+        const float* fQl = fF0 + (1 * kPNB + bx) * R8 * kPBC;
+        const float* fLh = fF0 + (2 * kPNB + bx) * R8 * kPBC;
+        const float* fLl = fF0 + (3 * kPNB + bx) * R8 * kPBC;
 #pragma unroll
-          for (int kb = 0; kb < KB; ++kb) {
-            const int o0 = offL0[j] + 256 * kb, o1 = offL1[j] + 256 * kb;
-            mma3(c, ah[kb], al[kb], lds_u32(fLh + o0), lds_u32(fLh + o1), lds_u32(fLl + o0),
-                 lds_u32(fLl + o1));
+        for (int jp = 0; jp < kPBC / 8; jp += 2) {
+          float x[2][4];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int j = jp + u;
+            // correction C = P_orth Q_loc^T (16 rows x 8 columns)
+            float c[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int kb = 0; kb < KB; ++kb) {
+              const int o0 = offL0[j] + 256 * kb, o1 = offL1[j] + 256 * kb;
+              mma3(c, ah[kb], al[kb], lds_u32(fLh + o0), lds_u32(fLh + o1), lds_u32(fLl + o0),
+                   lds_u32(fLl + o1));
+            }
+            const float2 m0 = *reinterpret_cast<const float2*>(sM + offX[j]);
+            const float2 m1 = *reinterpret_cast<const float2*>(sM + offX[j] + 256);
+            const float2 s0 = *reinterpret_cast<const float2*>(sS + offX[j]);
+            const float2 s1 = *reinterpret_cast<const float2*>(sS + offX[j] + 256);
+            x[u][0] = m0.x + s0.x - c[0];
+            x[u][1] = m0.y + s0.y - c[1];
+            x[u][2] = m1.x + s1.x - c[2];
+            x[u][3] = m1.y + s1.y - c[3];
           }
-          const float2 m0 = *reinterpret_cast<const float2*>(sM + offX[j]);
-          const float2 m1 = *reinterpret_cast<const float2*>(sM + offX[j] + 256);
-          const float2 s0 = *reinterpret_cast<const float2*>(sS + offX[j]);
-          const float2 s1 = *reinterpret_cast<const float2*>(sS + offX[j] + 256);
-          const float x0 = m0.x + s0.x - c[0], x1 = m0.y + s0.y - c[1];
-          const float x2 = m1.x + s1.x - c[2], x3 = m1.y + s1.y - c[3];
-          const int64_t col = c0 + colj[j];
           if (full) {
-            __stcs(reinterpret_cast<float2*>(Sa + col), make_float2(x0, x1));
-            __stcs(reinterpret_cast<float2*>(Sb + col), make_float2(x2, x3));
+            store_pair(Sa, Sb, c0 + colj[jp], c0 + colj[jp + 1], tq & 1, x[0], x[1]);
           } else {
-            const bool ca0 = col < m, ca1 = col + 1 < m;
-            if (oka && ca0) Sa[col] = x0;
-            if (oka && ca1) Sa[col + 1] = x1;
-            if (okb && ca0) Sb[col] = x2;
-            if (okb && ca1) Sb[col + 1] = x3;
+            store_own(Sa, Sb, c0 + colj[jp], m, oka, okb, x[0]);
+            store_own(Sa, Sb, c0 + colj[jp + 1], m, oka, okb, x[1]);
           }
-          // projection P += x Q_orth; A's k index t <-> column n = 2t, t + 4 <-> 2t + 1
-          uint32_t xh[4], xl[4];
-          split_tf32(x0, xh[0], xl[0]);
-          split_tf32(x2, xh[1], xl[1]);
-          split_tf32(x1, xh[2], xl[2]);
-          split_tf32(x3, xh[3], xl[3]);
 #pragma unroll
-          for (int nb = 0; nb < KB; ++nb) {
-            const int o = offQ[j] + 256 * nb;
-            const float2 bh = *reinterpret_cast<const float2*>(fQh + o);
-            const float2 bl = *reinterpret_cast<const float2*>(fQl + o);
-            mma3(pa[nb], xh, xl, __float_as_uint(bh.x), __float_as_uint(bh.y),
-                 __float_as_uint(bl.x), __float_as_uint(bl.y));
+          for (int u = 0; u < 2; ++u) {
+            const int j = jp + u;
+            // projection P += x Q_orth; A's k index t <-> column n = 2t, t + 4 <-> 2t + 1
+            uint32_t xh[4], xl[4];
+            split_tf32(x[u][0], xh[0], xl[0]);
+            split_tf32(x[u][2], xh[1], xl[1]);
+            split_tf32(x[u][1], xh[2], xl[2]);
+            split_tf32(x[u][3], xh[3], xl[3]);
+#pragma unroll
+            for (int nb = 0; nb < KB; ++nb) {
+              const int o = offQ[j] + 256 * nb;
+              const float2 bh = *reinterpret_cast<const float2*>(fQh + o);
+              const float2 bl = *reinterpret_cast<const float2*>(fQl + o);
+              mma3(pa[nb], xh, xl, __float_as_uint(bh.x), __float_as_uint(bh.y),
+                   __float_as_uint(bl.x), __float_as_uint(bl.y));
+            }
           }
+        }
         }
 #pragma unroll
         for (int kb = 0; kb < KB; ++kb) {
@@ -324,7 +414,7 @@ __device__ void tcq_producer(const Tables& t, const TcSeg* segs, int sb, int se,
     const int nbox = q_nbox(mp.pc);
     const int tr = mp.tr;
     const bool v16 = (m % 4 == 0) && ((reinterpret_cast<uintptr_t>(grad) & 15u) == 0);
-    const CUtensorMap* maps = t.tmaps + 8 * (int64_t)s.layer + 6;  // M, S with tr-row boxes
+    const CUtensorMap* maps = t.tmaps + 9 * (int64_t)s.layer + 6;  // M, S with tr-row boxes
     if (v16 && lane < 2) tmap_acquire(maps + lane);
     const float* fr[4] = {t.plsplit + L.ps_off, t.plsplit + L.ps_off + n * R8,
                           t.psplit + L.ps_off, t.psplit + L.ps_off + n * R8};
@@ -380,6 +470,7 @@ __device__ void tcq_consumer(const Tables& t, const TcSeg* segs, int sb, int se,
   const int g = lane >> 2, tq = lane & 3;
   int stage = 0;
   uint32_t phase = 0;
+  StageRelease rel;
   for (int si = sb; si < se; ++si) {
     const TcSeg s = segs[si];
     const LayerDesc& L = t.layers[s.layer];
@@ -401,6 +492,10 @@ __device__ void tcq_consumer(const Tables& t, const TcSeg* segs, int sb, int se,
     const int ksteps = tr / 8;
     const float* Qh = t.qsplit + L.qs_off;   // Q_orth [2][R8][m]
     const float* Ql = Qh + (int64_t)R8 * m;
+    // S is written back through shared memory + TMA store (map 7) when rows
+    // are 16-byte aligned; otherwise each lane stores its own elements
+    const bool tst = (m % 4 == 0);
+    const CUtensorMap* smap = t.tmaps + 9 * (int64_t)s.layer + 7;
     // this warp's column blocks (16 columns each) inside the panel
     uint32_t ah[CBW][KB][4], al[CBW][KB][4];
     float acc[CBW][KB][4];
@@ -435,7 +530,7 @@ __device__ void tcq_consumer(const Tables& t, const TcSeg* segs, int sb, int se,
     for (int64_t r0 = s.row0; r0 < s.row1; r0 += tr) {
       mbar_wait(&sh.full[stage], phase);
       const float* sM = sh.ring + (size_t)stage * sh.stage_floats;
-      const float* sS = sM + nbox * tr * 32;
+      float* sS = sh.ring + (size_t)stage * sh.stage_floats + nbox * tr * 32;
       const float* fLh = sS + nbox * tr * 32;   // P_loc hi [tr][RS]
       const float* fLl = fLh + tr * RS;
       const float* fPh = fLl + tr * RS;   // P_orth hi
@@ -478,7 +573,12 @@ __device__ void tcq_consumer(const Tables& t, const TcSeg* segs, int sb, int se,
           const float x2 = sM[offb[j] + ko] + sS[offb[j] + ko] - c[2];
           const float x3 = sM[offb1[j] + ko] + sS[offb1[j] + ko] - c[3];
           const int ca = (cg * CBW + j) * 16 + g, cb2 = ca + 8;
-          if (full) {
+          if (tst) {  // back into the S tile; the tile is stored by TMA below
+            sS[offa[j] + ko] = x0;
+            sS[offa1[j] + ko] = x1;
+            sS[offb[j] + ko] = x2;
+            sS[offb1[j] + ko] = x3;
+          } else if (full) {
             __stcs(Sa + ca, x0);
             __stcs(Sb + ca, x1);
             __stcs(Sa + cb2, x2);
@@ -514,8 +614,16 @@ __device__ void tcq_consumer(const Tables& t, const TcSeg* segs, int sb, int se,
           acc[j][kb][2] += ta[j][kb][2];
           acc[j][kb][3] += ta[j][kb][3];
         }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sh.empty[stage]);
+      if (tst) fence_async_smem();
+      consumers_sync();
+      if (threadIdx.x == 0) {
+        if (tst) {
+          for (int b = 0; b < nbox; ++b) tma_store_2d(smap, sS + b * tr * 32, (int)(c0 + 32 * b), (int)r0);
+          rel.after_store(sh, stage);
+        } else {
+          rel.immediate(sh, stage);
+        }
+      }
       if (++stage == sh.stages) {
         stage = 0;
         phase ^= 1u;
@@ -539,12 +647,192 @@ __device__ void tcq_consumer(const Tables& t, const TcSeg* segs, int sb, int se,
       }
     }
   }
+  if (threadIdx.x == 0) rel.finish();
+}
+
+// ---- decode (K3 on the tensor cores): grad = scale * A B^T, tile = 128 rows
+// (one 16-row block per warp) x 32 columns. B (the m-side factor) streams in
+// as 128B-swizzled boxes of R8 x 32 floats: MODE 2 (P-step) reads Q_orth's
+// split copy (maps 2, 3), MODE 3 (Q-step) the all-reduced Q slot (map 8),
+// split on use. A: P-step the all-reduced P slot (split once per row block),
+// Q-step P_orth's split copy. Write-only: 4 B per element.
+constexpr int kDNB = 4;  // boxes per decode tile (128 rows x 128 columns)
+__host__ __device__ constexpr int d_stage_floats(int r8) { return 2 * kDNB * r8 * kPBC; }
+
+template <int MODE, int R8>
+__device__ void tcd_producer(const Tables& t, const TcSeg* segs, int sb, int se, const TcShared& sh) {
+  const int lane = threadIdx.x & 31;
+  uint64_t pol_keep;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
+  int stage = 0;
+  uint32_t phase = 0;
+  for (int si = sb; si < se; ++si) {
+    const TcSeg s = segs[si];
+    const LayerDesc& L = t.layers[s.layer];
+    if (!L.mat) continue;
+    const int64_t m = L.m;
+    const CUtensorMap* maps = t.tmaps + 9 * (int64_t)s.layer;
+    const bool v16 = (m % 4 == 0);
+    if (v16 && lane < 9) tmap_acquire(maps + lane);
+    const float* src0 = MODE == 2 ? t.qsplit + L.qs_off : t.qbuf + L.q_off;
+    const float* src1 = MODE == 2 ? t.qsplit + L.qs_off + (int64_t)R8 * m : nullptr;
+    const int rows_b = MODE == 2 ? R8 : L.r;  // rows present in the source array
+    for (int64_t r0 = s.row0; r0 < s.row1; r0 += kPTR) {
+      for (int64_t c0 = 0; c0 < m; c0 += kDNB * kPBC) {
+        if (lane == 0) mbar_wait(&sh.empty[stage], phase ^ 1u);
+        __syncwarp();
+        float* dB = sh.ring + (size_t)stage * sh.stage_floats;  // [array][box] of R8 x 32
+        if (v16) {
+          if (lane == 0) {
+            if constexpr (MODE == 2) {
+              mbar_arrive_tx(&sh.full[stage], 2u * kDNB * R8 * kPBC * 4u);
+              for (int b = 0; b < kDNB; ++b) {
+                tma_load_2d(dB + b * R8 * kPBC, maps + 2, (int)c0 + kPBC * b, 0, &sh.full[stage], pol_keep);
+                tma_load_2d(dB + (kDNB + b) * R8 * kPBC, maps + 3, (int)c0 + kPBC * b, 0, &sh.full[stage],
+                            pol_keep);
+              }
+            } else {
+              mbar_arrive_tx(&sh.full[stage], (uint32_t)kDNB * R8 * kPBC * 4u);
+              for (int b = 0; b < kDNB; ++b)
+                tma_load_2d(dB + b * R8 * kPBC, maps + 8, (int)c0 + kPBC * b, 0, &sh.full[stage], pol_keep);
+            }
+          }
+        } else {
+          if (lane == 0) mbar_arrive(&sh.full[stage]);
+          const int arrays = MODE == 2 ? 2 : 1;
+          for (int it = lane; it < arrays * R8 * kDNB * kPBC; it += 32) {
+            const int a = it / (R8 * kDNB * kPBC), rem = it - a * (R8 * kDNB * kPBC);
+            const int k = rem / (kDNB * kPBC), j = rem - k * (kDNB * kPBC);
+            const bool ok = k < rows_b && c0 + j < m;
+            const float* src = a == 0 ? src0 : src1;
+            cp_async4(dB + (a * kDNB + (j >> 5)) * R8 * kPBC + swz(k, (j & 31) >> 2) + (j & 3),
+                      src + (ok ? k * m + c0 + j : 0), ok ? 4u : 0u);
+          }
+        }
+        cp_async_arrive(&sh.full[stage]);
+        if (++stage == sh.stages) {
+          stage = 0;
+          phase ^= 1u;
+        }
+      }
+    }
+  }
+}
+
+template <int MODE, int R8>
+__device__ void tcd_consumer(const Tables& t, const TcSeg* segs, int sb, int se, const TcShared& sh,
+                             float scale) {
+  constexpr int KB = R8 / 8;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, tq = lane & 3;
+  const int rw = 16 * warp + g;
+  int offL0[4], offL1[4], colj[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int cj = tq < 2 ? j : j + 4, oc = 2 * (tq & 1);
+    const int cg = g < 4 ? j : j + 4, og = g & 3;
+    offL0[j] = swz(tq, cg) + og;      // + 256 * kb (rows 8kb + tq)
+    offL1[j] = swz(tq + 4, cg) + og;  // rows 8kb + tq + 4
+    colj[j] = 4 * cj + oc;
+  }
+  int stage = 0;
+  uint32_t phase = 0;
+  for (int si = sb; si < se; ++si) {
+    const TcSeg s = segs[si];
+    const LayerDesc& L = t.layers[s.layer];
+    float* grad = t.grads[s.layer];
+    if (!L.mat) {  // vector: unpack from the parity's buffer
+      const float* slot = (MODE == 2 ? t.pbuf + L.p_off : t.qbuf + L.q_off);
+      for (int64_t i = s.row0 + threadIdx.x; i < s.row1; i += kTcNW * 32) grad[i] = slot[i] * scale;
+      continue;
+    }
+    const int64_t m = L.m, n = L.n;
+    const int r = L.r;
+    const bool v4 = (m % 4 == 0) && ((reinterpret_cast<uintptr_t>(grad) & 15u) == 0);
+    for (int64_t r0 = s.row0; r0 < s.row1; r0 += kPTR) {
+      const int64_t ra = r0 + rw, rb = ra + 8;
+      const bool oka = ra < s.row1, okb = rb < s.row1;
+      uint32_t ah[KB][4], al[KB][4];
+#pragma unroll
+      for (int kb = 0; kb < KB; ++kb) {
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const int k = 8 * kb + tq + ((h & 2) ? 4 : 0);
+          const int64_t row = (h & 1) ? rb : ra;
+          const bool ok = ((h & 1) ? okb : oka) && k < r;
+          if constexpr (MODE == 2) {  // all-reduced P slot, k-major fp32: split here
+            const float v = ok ? t.pbuf[L.p_off + (int64_t)k * n + row] * scale : 0.f;
+            split_tf32(v, ah[kb][h], al[kb][h]);
+          } else {                    // P_orth split copy [2][n][R8]
+            const float* Ps = t.psplit + L.ps_off;
+            ah[kb][h] = ok ? __float_as_uint(Ps[row * R8 + k] ) : 0u;
+            al[kb][h] = ok ? __float_as_uint(Ps[(n + row) * R8 + k]) : 0u;
+          }
+        }
+      }
+      float* Ga = grad + ra * m;
+      float* Gb = grad + rb * m;
+      const bool rows_full = r0 + kPTR <= s.row1;
+      for (int64_t c00 = 0; c00 < m; c00 += kDNB * kPBC) {
+        mbar_wait(&sh.full[stage], phase);
+        const float* fB0 = sh.ring + (size_t)stage * sh.stage_floats;
+        const bool full = rows_full && (c00 + kDNB * kPBC <= m) && v4;
+#pragma unroll
+        for (int bx = 0; bx < kDNB; ++bx) {
+        const int64_t c0 = c00 + kPBC * bx;
+        const float* fBh = fB0 + bx * R8 * kPBC;
+        const float* fBl = fB0 + (kDNB + bx) * R8 * kPBC;
+#pragma unroll
+        for (int jp = 0; jp < kPBC / 8; jp += 2) {
+        float cc[2][4];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int j = jp + u;
+          float (&c)[4] = cc[u];
+          c[0] = c[1] = c[2] = c[3] = 0.f;
+#pragma unroll
+          for (int kb = 0; kb < KB; ++kb) {
+            const int o0 = offL0[j] + 256 * kb, o1 = offL1[j] + 256 * kb;
+            uint32_t bh0, bh1, bl0, bl1;
+            if constexpr (MODE == 2) {
+              bh0 = lds_u32(fBh + o0);
+              bh1 = lds_u32(fBh + o1);
+              bl0 = lds_u32(fBl + o0);
+              bl1 = lds_u32(fBl + o1);
+            } else {
+              split_tf32(fBh[o0], bh0, bl0);
+              split_tf32(fBh[o1], bh1, bl1);
+            }
+            mma3(c, ah[kb], al[kb], bh0, bh1, bl0, bl1);
+          }
+          if constexpr (MODE == 3) {
+#pragma unroll
+            for (int h = 0; h < 4; ++h) c[h] *= scale;
+          }
+        }
+        if (full) {
+          store_pair(Ga, Gb, c0 + colj[jp], c0 + colj[jp + 1], tq & 1, cc[0], cc[1]);
+        } else {
+          store_own(Ga, Gb, c0 + colj[jp], m, oka, okb, cc[0]);
+          store_own(Ga, Gb, c0 + colj[jp + 1], m, oka, okb, cc[1]);
+        }
+        }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sh.empty[stage]);
+        if (++stage == sh.stages) {
+          stage = 0;
+          phase ^= 1u;
+        }
+      }
+    }
+  }
 }
 
 template <int MODE, int R8>
 __global__ void __launch_bounds__(kTcNW * 32 + 32, 1)
 tc_kernel(Tables t, const TcSeg* __restrict__ segs, const int32_t* __restrict__ cta_begin,
-          int stages, int stage_floats) {
+          int stages, int stage_floats, float scale) {
   extern __shared__ __align__(1024) unsigned char tc_smem_raw[];  // SWIZZLE_128B boxes
   TcShared sh;
   sh.stages = stages;
@@ -556,7 +844,8 @@ tc_kernel(Tables t, const TcSeg* __restrict__ segs, const int32_t* __restrict__ 
   if (threadIdx.x == 0) {
     for (int i = 0; i < stages; ++i) {
       mbar_init(&sh.full[i], 33);      // lane 0's expect-tx arrive + one noinc arrive per lane
-      mbar_init(&sh.empty[i], kTcNW);  // one arrive per consumer warp
+      // Q-step K1: consumer thread 0 releases (after the S store read it); else one per warp
+      mbar_init(&sh.empty[i], MODE == 1 ? 1 : kTcNW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -566,9 +855,12 @@ tc_kernel(Tables t, const TcSeg* __restrict__ segs, const int32_t* __restrict__ 
   if constexpr (MODE == 0) {
     if (producer) tcp_producer<R8>(t, segs, sb, se, sh);
     else tcp_consumer<R8>(t, segs, sb, se, sh);
-  } else {
+  } else if constexpr (MODE == 1) {
     if (producer) tcq_producer<R8>(t, segs, sb, se, sh);
     else tcq_consumer<R8, (R8 <= 16 ? 2 : 1)>(t, segs, sb, se, sh);
+  } else {
+    if (producer) tcd_producer<MODE, R8>(t, segs, sb, se, sh);
+    else tcd_consumer<MODE, R8>(t, segs, sb, se, sh, scale);
   }
 }
 
@@ -601,7 +893,7 @@ int tc_q_map(int64_t m, int r8, TcMap* out) {
   const int64_t maxpc = (int64_t)16 * cbw * kTcNW;
   const int64_t np = (m + maxpc - 1) / maxpc;
   int64_t pc = (m + np - 1) / np;
-  pc = (pc + 15) / 16 * 16;
+  pc = (pc + 31) / 32 * 32;  // whole 32-column boxes: the S store never touches another panel
   const int ncb = (int)(pc / 16);
   const int need = (ncb + cbw - 1) / cbw;
   int wc = 1;
@@ -653,13 +945,13 @@ bool tc_encode_map(CUtensorMap* out, const float* base, int64_t cols, int64_t ro
 int tc_p_box_rows() { return kPTR; }
 
 cudaError_t launch_tc(int mode, int r8, const Tables& t, const TcSeg* segs, const int32_t* cb, int ncta,
-                      int stages, int stage_floats, cudaStream_t st) {
+                      int stages, int stage_floats, float scale, cudaStream_t st) {
   if (ncta <= 0) return cudaSuccess;
   const size_t smem = tc_smem_bytes(stages, stage_floats);
   auto go = [&](auto kern) -> cudaError_t {
     cudaError_t e = allow_max_smem(reinterpret_cast<const void*>(kern));
     if (e != cudaSuccess) return e;
-    kern<<<ncta, kTcNW * 32 + 32, smem, st>>>(t, segs, cb, stages, stage_floats);
+    kern<<<ncta, kTcNW * 32 + 32, smem, st>>>(t, segs, cb, stages, stage_floats, scale);
     return cudaGetLastError();
   };
   switch (mode * 100 + r8) {
@@ -669,9 +961,17 @@ cudaError_t launch_tc(int mode, int r8, const Tables& t, const TcSeg* segs, cons
     case 108: return go(tc_kernel<1, 8>);
     case 116: return go(tc_kernel<1, 16>);
     case 132: return go(tc_kernel<1, 32>);
+    case 208: return go(tc_kernel<2, 8>);
+    case 216: return go(tc_kernel<2, 16>);
+    case 232: return go(tc_kernel<2, 32>);
+    case 308: return go(tc_kernel<3, 8>);
+    case 316: return go(tc_kernel<3, 16>);
+    case 332: return go(tc_kernel<3, 32>);
     default: return cudaErrorInvalidValue;
   }
 }
+
+int tc_d_stage_floats(int r8) { return d_stage_floats(r8); }
 
 cudaError_t launch_tc_materialize(const Tables& t, const LayerDesc& L, int which, float* dst,
                                   cudaStream_t s) {
