@@ -139,6 +139,32 @@ def oracle_sample(model, rank, frac_every=3):
     return out
 
 
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def time_oracle_threads(model, rank, steps, warmup, frac_every=3):
+    """The oracle on 1 thread and on all host cores."""
+    out = {}
+    try:
+        from threadpoolctl import threadpool_limits
+    except Exception:
+        threadpool_limits = None
+    for label, limit in (("1_thread", 1), ("all_cores", None)):
+        if threadpool_limits is not None and limit is not None:
+            with threadpool_limits(limits=limit):
+                out[label] = time_oracle(model, rank, steps, warmup, frac_every=frac_every)
+        else:
+            out[label] = time_oracle(model, rank, steps, warmup, frac_every=frac_every)
+    return out
+
+
 def time_oracle(model, rank, steps, warmup, world=1, frac_every=3):
     """Run the oracle (as it stands) on the bounded sample; returns GB/s."""
     import numpy as np
@@ -172,6 +198,7 @@ def run_reference(args):
         "config": {"workload": args.workload, "rank": r, "sample_elements": res["elements"],
                    "sample_tensors": res["tensors"]},
         "cpu_baseline": {"value": res["gbs"], "unit": "GB/s", "cores": cores, "kind": "oracle",
+                         "cpu_model": _cpu_model(),
                          "sample": f"{model} r={r}: every {args.oracle_every}-th matrix + all vectors "
                                    f"({res['elements']} elements), one worker, numpy fp64"},
         "e2e": {"value": res["gbs"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -229,20 +256,28 @@ def _measure(model, r, world, rank, local, args, comm, profile=True, flags=0):
     if world > 1:
         torch.distributed.barrier()
     l0 = ctx.launch_count()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         if world > 1:
             torch.distributed.barrier()
-        ev0.record(stream)
+        evs[0].record(stream)
         for t in range(args.steps):
             ctx.step(grads, (args.warmup + t) % 2)
-        ev1.record(stream)
+            evs[t + 1].record(stream)
         torch.cuda.synchronize()
         if world > 1:
             torch.distributed.barrier()
     launches = ctx.launch_count() - l0
-    ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
+    ms = max_over_ranks(evs[0].elapsed_time(evs[-1]) / args.steps)
+    per = [evs[t].elapsed_time(evs[t + 1]) for t in range(args.steps)]
+    par = [(args.warmup + t) % 2 for t in range(args.steps)]
+    pm = [x for x, q in zip(per, par) if q == 0]
+    qm = [x for x, q in zip(per, par) if q == 1]
+    import statistics
+    step_stats = {"mean_ms": statistics.fmean(per), "std_ms": statistics.pstdev(per),
+                  "p_step_ms": max_over_ranks(statistics.fmean(pm)) if pm else None,
+                  "q_step_ms": max_over_ranks(statistics.fmean(qm)) if qm else None}
     prof = None
     if profile:
         # per-kernel CUDA events on the launching stream (eager launches)
@@ -255,7 +290,36 @@ def _measure(model, r, world, rank, local, args, comm, profile=True, flags=0):
         ctx.profile(False)
     nb = (len(ctx.buckets(0)), len(ctx.buckets(1)))
     return {"ctx": ctx, "grads": grads, "shapes": shapes, "nel": nel, "ms": ms, "prof": prof,
-            "launches": launches, "clocks": clk.summary(), "buckets": nb}
+            "launches": launches, "clocks": clk.summary(), "buckets": nb, "step_stats": step_stats}
+
+
+def _ssgd(nel, world, args):
+    """NEXT-4 context: the dense S-SGD exchange of the same gradient set, a
+    plain NCCL all-reduce (sum) in 25 MiB buckets, max over ranks."""
+    import torch
+    import torch.distributed as dist
+    flat = torch.zeros(nel, dtype=torch.float32, device="cuda")
+    bucket = 25 * 2 ** 20 // 4
+    chunks = [flat[i:i + bucket] for i in range(0, nel, bucket)]
+    for _ in range(2):
+        for c in chunks:
+            dist.all_reduce(c)
+    torch.cuda.synchronize()
+    dist.barrier()
+    steps = max(3, min(args.steps, 10))
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(steps):
+        for c in chunks:
+            dist.all_reduce(c)
+    ev1.record()
+    torch.cuda.synchronize()
+    ms = max_over_ranks(ev0.elapsed_time(ev1) / steps)
+    busbw = 2.0 * (world - 1) / world * 4.0 * nel / (ms * 1e-3) / 1e9
+    del flat, chunks
+    torch.cuda.empty_cache()
+    return {"ms_per_step": ms, "buckets": (nel + bucket - 1) // bucket, "busbw_gbs": busbw,
+            "nvlink_frac": busbw / 900.0}
 
 
 def _e2e(res, world, args):
@@ -289,6 +353,18 @@ def _e2e(res, world, args):
     nbytes = 4 * res["nel"]
     return {"value": world * nbytes / (ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": ms,
             "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "steps": steps}
+
+
+def _nvlink(prof, world):
+    """All-reduce bus bandwidth 2(p-1)/p * bytes / t of the eager profiled pass
+    against 900 GB/s per direction (NVLink 5), SURVEY §8(d)."""
+    if world <= 1 or not prof or prof.get("allreduce", {}).get("launches", 0) == 0:
+        return None
+    a = prof["allreduce"]
+    t = a["ms"] / a["launches"] * 1e-3
+    b = a["bytes"] / a["launches"]
+    bus = 2.0 * (world - 1) / world * b / t / 1e9
+    return {"busbw_gbs": bus, "frac_900": bus / 900.0, "bytes_per_group": b, "ms_per_group": t * 1e3}
 
 
 def _roofline(prof, peak, peak_kind, workload):
@@ -355,10 +431,16 @@ def run_ours(args):
                 "acp_speedup": ps["ms"] / ms, "gpu_launches": ps["launches"]}
         ps["ctx"].close()
         del ps
+    ssgd = None
+    if world > 1 and not args.no_ssgd:
+        ssgd = _ssgd(nel, world, args)
+        ssgd["acp_speedup"] = ssgd["ms_per_step"] / ms
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cb = time_oracle(model, r, 2, 1, frac_every=args.oracle_every)
+        cbt = time_oracle_threads(model, r, 2, 1, frac_every=args.oracle_every)
+        cb = cbt["all_cores"]
         cpu = {"value": cb["gbs"], "unit": "GB/s", "cores": _cpu_threads(), "kind": "oracle",
+               "cpu_model": _cpu_model(), "value_1_thread": cbt["1_thread"]["gbs"],
                "sample": f"{model} r={r}: every {args.oracle_every}-th matrix + all vectors "
                          f"({cb['elements']} of {nel} elements), 1 warm + 2 timed steps (P,Q), numpy fp64"}
     if rank == 0:
@@ -374,6 +456,8 @@ def run_ours(args):
                        "l2": "inputs larger than L2 (M+E working set > 126 MB), no flush",
                        "parallelism": f"dp{world}"},
             "step_hbm_frac_16B": 16.0 * nel / (ms * 1e-3) / 1e9 / peak,
+            "step_stats": res["step_stats"],
+            "nvlink": _nvlink(res["prof"], world),
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,
@@ -381,6 +465,7 @@ def run_ours(args):
             "gpu_launches": res["launches"],
             "secondary": secondary,
             "powersgd": psgd,
+            "ssgd": ssgd,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -404,6 +489,8 @@ def main(argv=None):
     ap.add_argument("--no-graphs", action="store_true")
     ap.add_argument("--no-powersgd", action="store_true",
                     help="skip the on-box Power-SGD comparison line")
+    ap.add_argument("--no-ssgd", action="store_true",
+                    help="skip the dense S-SGD all-reduce comparison (N > 1)")
     ap.add_argument("--oracle-every", type=int, default=3)
     args = ap.parse_args(argv)
     if args.warmup < 3:
