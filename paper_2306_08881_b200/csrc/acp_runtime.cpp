@@ -98,7 +98,7 @@ struct Plan {
 
 // Split `units` into `grid` contiguous, cost-balanced CTA ranges of segments.
 template <class Emit>
-int split_units(const std::vector<Unit>& units, double min_share, int max_grid,
+int split_units(const std::vector<Unit>& units, int nsm, double min_share, int max_grid,
                 std::vector<int32_t>& ctab, Emit emit) {
   double total = 0;
   for (const Unit& u : units) total += u.cost * (double)u.count;
@@ -108,6 +108,9 @@ int split_units(const std::vector<Unit>& units, double min_share, int max_grid,
   }
   int grid = (int)std::ceil(total / min_share);
   grid = std::max(1, std::min(grid, max_grid));
+  // whole waves: a multiple of the SM count (max_grid is one), so every SM
+  // gets the same number of equal shares
+  if (grid > nsm && nsm > 0) grid = std::min(max_grid, (grid + nsm - 1) / nsm * nsm);
   const double share = total / grid;
   const size_t cb0 = ctab.size();
   int nseg = 0;
@@ -300,7 +303,9 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
       const double bpe = mode == 0 ? (ef ? 12.0 : 4.0) : ((mode == 1 || mode == 3) ? 4.0 : (ef ? 16.0 : 8.0));
       int64_t align = 1;
       if (L.G > 0) align = (int64_t)(kThreads / L.G) * row_rows_per_iter(mode, L.V, P.RT);
-      units.push_back({i, -1, L.n, bpe * (double)L.m, align});
+      // balance by expected time, not bytes: the generic path is several
+      // times slower per byte (it set the tail of ResNet-50's conv1)
+      units.push_back({i, -1, L.n, bpe * (double)L.m * (L.G > 0 ? 1.0 : 6.0), align});
       // algorithmic bytes: M/E stream + factor traffic (each factor touched once)
       bytes += bpe * (double)L.n * (double)L.m;
       if (mode == 0) bytes += 4.0 * L.r * (double)(L.m + L.n);
@@ -312,7 +317,7 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
     ln.mode = mode;
     ln.seg_off = (int64_t)P.rowsegs.size();
     ln.cb_off = (int64_t)P.ctab.size();
-    ln.ncta = split_units(units, min_share, max_grid, P.ctab, [&](const Unit& u, int64_t a, int64_t b) {
+    ln.ncta = split_units(units, nsm, min_share, max_grid, P.ctab, [&](const Unit& u, int64_t a, int64_t b) {
       RowSeg s{};
       s.layer = u.layer;
       s.row0 = a;
@@ -353,7 +358,7 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
       const int cnt = (int)(P.colsegs.size() - panel_first);
       for (size_t k = panel_first; k < P.colsegs.size(); ++k) P.colsegs[k].pcount = cnt;
     };
-    ln.ncta = split_units(units, min_share, max_grid, P.ctab, [&](const Unit& u, int64_t a, int64_t b) {
+    ln.ncta = split_units(units, nsm, min_share, max_grid, P.ctab, [&](const Unit& u, int64_t a, int64_t b) {
       ColSeg s{};
       s.layer = u.layer;
       s.panel = u.panel;
@@ -416,7 +421,9 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
         factor_floats = std::max<int64_t>(factor_floats, (int64_t)P.RT * L.m);
       for (int pn = 0; pn < np; ++pn) {
         const int64_t cols = std::min<int64_t>(pc, L.m - (int64_t)pn * pc);
-        units.push_back({i, pn, L.n, bpe * (double)cols, tr});
+        // time-weighted cost (generic path ~8x, sub-warp rows ~2x per byte)
+        const double mult = fast ? (mp.lg < 32 ? 2.0 : 1.0) : 8.0;
+        units.push_back({i, pn, L.n, bpe * (double)cols * mult, tr});
       }
       bytes += bpe * (double)L.n * (double)L.m;
       if (mode == 0) bytes += 4.0 * L.r * (double)(L.m + L.n);
@@ -447,7 +454,7 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
     int64_t part = 0;
     int prev_layer = -1, prev_panel = -1;
     ln.red_off = (int64_t)P.redtasks.size();
-    ln.ncta = split_units(units, min_share, nsm * cps * stream_waves, P.ctab, [&](const Unit& u, int64_t a, int64_t b) {
+    ln.ncta = split_units(units, nsm, min_share, nsm * cps * stream_waves, P.ctab, [&](const Unit& u, int64_t a, int64_t b) {
       StreamSeg s{};
       s.layer = u.layer;
       s.row0 = a;
@@ -509,17 +516,17 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
       }
       if (mode >= 2) {  // decode: grad written (+ the two factors once)
         bytes += 4.0 * (double)L.n * (double)L.m + 4.0 * L.r * (double)(L.n + L.m);
-        units.push_back({i, -1, L.n, 4.0 * (double)L.m, 128});
+        units.push_back({i, -1, L.n, 4.0 * (double)L.m * (L.m % 4 ? 6.0 : 1.0), 128});
         continue;
       }
       // algorithmic bytes: M, S read, S written + the factors once
       bytes += 12.0 * (double)L.n * (double)L.m + 4.0 * L.r * (2.0 * L.n + 2.0 * L.m);
       if (mode == 0) {
-        units.push_back({i, -1, L.n, 12.0 * (double)L.m, 128});
+        units.push_back({i, -1, L.n, 12.0 * (double)L.m * (L.m % 4 ? 6.0 : 1.0), 128});
       } else {
         for (int pn = 0; pn < L.tq.np; ++pn) {
           const int64_t cols = std::min<int64_t>(L.tq.pc, L.m - (int64_t)pn * L.tq.pc);
-          units.push_back({i, pn, L.n, 12.0 * (double)cols, L.tq.tr});
+          units.push_back({i, pn, L.n, 12.0 * (double)cols * (L.m % 4 ? 6.0 : 1.0), L.tq.tr});
         }
       }
     }
@@ -536,7 +543,7 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
     int64_t part = 0;
     int prev_layer = -1, prev_panel = -1;
     ln.red_off = (int64_t)P.redtasks.size();
-    ln.ncta = split_units(units, min_share, nsm, P.ctab, [&](const Unit& u, int64_t a, int64_t b) {
+    ln.ncta = split_units(units, nsm, min_share, nsm, P.ctab, [&](const Unit& u, int64_t a, int64_t b) {
       TcSeg sg{};
       sg.layer = u.layer;
       sg.row0 = a;

@@ -187,6 +187,7 @@ __global__ void __launch_bounds__(kThreads) col_kernel(Tables t, const ColSeg* _
   __shared__ __align__(16) float red[kThreads * 32];
   __shared__ int flag;
   const int sb = cta_begin[blockIdx.x], se = cta_begin[blockIdx.x + 1];
+  prefetch_segs(t, segs, sb, se);
   for (int si = sb; si < se; ++si) {
     const ColSeg s = segs[si];
     const LayerDesc L = t.layers[s.layer];

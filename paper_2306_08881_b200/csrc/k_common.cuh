@@ -128,6 +128,48 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src, uint32_t 
                : "memory");
 }
 
+// Warm L1 with the descriptors a CTA's work segments refer to (segment,
+// LayerDesc, gradient pointer), one round trip for all of them: each segment
+// otherwise starts with a chain of dependent loads (segment -> layer ->
+// gradient pointer), which dominated models with many small layers.
+template <class Seg>
+__device__ __forceinline__ void prefetch_segs(const Tables& t, const Seg* segs, int sb, int se) {
+  for (int i = sb + (int)threadIdx.x; i < se; i += (int)blockDim.x) {
+    const int layer = segs[i].layer;
+    const char* L = reinterpret_cast<const char*>(t.layers + layer);
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(L));
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(L + 128));
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(L + sizeof(LayerDesc) - 1));
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(t.grads + layer));
+  }
+}
+
+// A run of consecutive vector (1-D) segments starting at s. Short segments
+// are spread over the warps (warp w takes every nwarps-th one, lanes stride
+// its elements), so the run's small tensors are in flight together instead
+// of costing one memory round trip each; long ones (>= 64 elements per warp)
+// use the whole CTA. f(seg, layer, first, stride) walks elements
+// [row0 + first, row1) with the given stride. Returns the index of the first
+// non-vector segment.
+template <class Seg, class F>
+__device__ __forceinline__ int vector_run(const Tables& t, const Seg* segs, int s, int se, int warp,
+                                          int nwarps, F&& f) {
+  const int lane = threadIdx.x & 31, nt = 32 * nwarps;
+  int e = s, k = 0;
+  for (; e < se; ++e) {
+    const Seg sg = segs[e];
+    const LayerDesc& L = t.layers[sg.layer];
+    if (L.mat) break;
+    if (sg.row1 - sg.row0 >= 64 * nwarps) {
+      f(sg, L, (int)threadIdx.x, nt);
+    } else {
+      if (k == warp) f(sg, L, lane, 32);
+      if (++k == nwarps) k = 0;
+    }
+  }
+  return e;
+}
+
 constexpr int kTagQ0 = 1, kTagDegenerate = 2, kTagNoReuse = 3;
 
 // 3xTF32: x = hi + lo with hi = x rounded to TF32 (10-bit

@@ -381,19 +381,24 @@ __global__ void __launch_bounds__(kThreads) row_kernel(Tables t, const RowSeg* _
   // Q-step residual (k_stream.cu): E is materialised again
   if (MODE == 1 && blockIdx.x == 0 && threadIdx.x == 0) *t.deferred = 0;
   const int sb = cta_begin[blockIdx.x], se = cta_begin[blockIdx.x + 1];
+  prefetch_segs(t, segs, sb, se);
   for (int s = sb; s < se; ++s) {
+    if (!t.layers[segs[s].layer].mat) {
+      // vectors: pack (mode 0) into the P-buffer / unpack (modes 1, 2, 3)
+      s = vector_run(t, segs, s, se, threadIdx.x >> 5, kThreads / 32,
+                     [&](const RowSeg& sg, const LayerDesc& L, int first, int stride) {
+                       float* grad = t.grads[sg.layer];
+                       float* slot = (MODE >= 2 ? t.qbuf + L.q_off : t.pbuf + L.p_off);
+                       for (int64_t i = sg.row0 + first; i < sg.row1; i += stride) {
+                         if (MODE == 0) slot[i] = grad[i];
+                         else grad[i] = slot[i] * scale;
+                       }
+                     }) - 1;
+      continue;
+    }
     const RowSeg sg = segs[s];
     const LayerDesc L = t.layers[sg.layer];
     float* grad = t.grads[sg.layer];
-    if (!L.mat) {
-      // vectors: pack (mode 0) into the P-buffer / unpack (modes 1, 2)
-      float* slot = (MODE >= 2 ? t.qbuf + L.q_off : t.pbuf + L.p_off);
-      for (int64_t i = sg.row0 + threadIdx.x; i < sg.row1; i += kThreads) {
-        if (MODE == 0) slot[i] = grad[i];
-        else grad[i] = slot[i] * scale;
-      }
-      continue;
-    }
     const bool fast = L.G > 0 && ((reinterpret_cast<uintptr_t>(grad) & 15u) == 0);
     if (!fast) {
       row_generic<MODE == 3 ? 1 : MODE, RT>(t, L, grad, sg.row0, sg.row1, scale, ef, red_gen);

@@ -716,6 +716,7 @@ __global__ void __launch_bounds__(nw_of(MODE, RT) * 32 + 32, Cfg<MODE>::CPS)
   }
   __syncthreads();
   const int sb = cta_begin[blockIdx.x], se = cta_begin[blockIdx.x + 1];
+  prefetch_segs(t, segs, sb, se);
   // deferred Q-step residual: K1 Q-step raises the flag (nothing in that
   // launch reads it); K1 P-step reads it (cleared later by the P decode)
   // defer bit 1 (mode 0): projection only, no residual (Power-SGD, whose
@@ -732,22 +733,23 @@ __global__ void __launch_bounds__(nw_of(MODE, RT) * 32 + 32, Cfg<MODE>::CPS)
   Pipe pp;
   int rph = 0;
   for (int si = sb; si < se; ++si) {
+    if (!t.layers[segs[si].layer].mat) {
+      si = vector_run(t, segs, si, se, threadIdx.x >> 5, NT / 32,
+                      [&](const StreamSeg& s, const LayerDesc& L, int first, int stride) {
+                        float* grad = t.grads[s.layer];
+                        if (MODE == 0 || MODE == 3) {
+                          float* slot = (MODE == 0 ? t.pbuf + L.p_off : t.qbuf + L.q_off);
+                          for (int64_t i = s.row0 + first; i < s.row1; i += stride) slot[i] = grad[i];
+                        } else {
+                          const float* slot = t.qbuf + L.q_off;
+                          for (int64_t i = s.row0 + first; i < s.row1; i += stride) grad[i] = slot[i] * scale;
+                        }
+                      }) - 1;
+      continue;
+    }
     const StreamSeg s = segs[si];
     const LayerDesc& L = t.layers[s.layer];
     float* grad = t.grads[s.layer];
-    if (!L.mat) {
-      if (MODE == 0) {
-        float* slot = t.pbuf + L.p_off;
-        for (int64_t i = s.row0 + threadIdx.x; i < s.row1; i += NT) slot[i] = grad[i];
-      } else if (MODE == 3) {
-        float* slot = t.qbuf + L.q_off;
-        for (int64_t i = s.row0 + threadIdx.x; i < s.row1; i += NT) slot[i] = grad[i];
-      } else {
-        const float* slot = t.qbuf + L.q_off;
-        for (int64_t i = s.row0 + threadIdx.x; i < s.row1; i += NT) grad[i] = slot[i] * scale;
-      }
-      continue;
-    }
     if (!is_fast<MODE>(L, grad)) {
       seg_generic<MODE, RT>(t, L, s, grad, scale, sh.gred, MODE == 0 ? (dflag | (projonly << 1)) : defer);
     } else {

@@ -235,14 +235,17 @@ __device__ void tcp_consumer(const Tables& t, const TcSeg* segs, int sb, int se,
   int stage = 0;
   uint32_t phase = 0;
   for (int si = sb; si < se; ++si) {
+    if (!t.layers[segs[si].layer].mat) {  // vectors: pack into the P-buffer slots
+      si = vector_run(t, segs, si, se, warp, kTcNW, [&](const TcSeg& s, const LayerDesc& L, int first, int stride) {
+             const float* grad = t.grads[s.layer];
+             float* slot = t.pbuf + L.p_off;
+             for (int64_t i = s.row0 + first; i < s.row1; i += stride) slot[i] = grad[i];
+           }) - 1;
+      continue;
+    }
     const TcSeg s = segs[si];
     const LayerDesc& L = t.layers[s.layer];
     float* grad = t.grads[s.layer];
-    if (!L.mat) {  // vector: pack into the P-buffer slot
-      float* slot = t.pbuf + L.p_off;
-      for (int64_t i = s.row0 + threadIdx.x; i < s.row1; i += kTcNW * 32) slot[i] = grad[i];
-      continue;
-    }
     const int64_t m = L.m, n = L.n;
     const int r = L.r;
     float* S = t.E + L.e_off;
@@ -472,14 +475,17 @@ __device__ void tcq_consumer(const Tables& t, const TcSeg* segs, int sb, int se,
   uint32_t phase = 0;
   StageRelease rel;
   for (int si = sb; si < se; ++si) {
+    if (!t.layers[segs[si].layer].mat) {  // vectors: pack into the Q-buffer slots
+      si = vector_run(t, segs, si, se, warp, kTcNW, [&](const TcSeg& s, const LayerDesc& L, int first, int stride) {
+             const float* grad = t.grads[s.layer];
+             float* slot = t.qbuf + L.q_off;
+             for (int64_t i = s.row0 + first; i < s.row1; i += stride) slot[i] = grad[i];
+           }) - 1;
+      continue;
+    }
     const TcSeg s = segs[si];
     const LayerDesc& L = t.layers[s.layer];
     float* grad = t.grads[s.layer];
-    if (!L.mat) {  // vector: pack into the Q-buffer slot
-      float* slot = t.qbuf + L.q_off;
-      for (int64_t i = s.row0 + threadIdx.x; i < s.row1; i += kTcNW * 32) slot[i] = grad[i];
-      continue;
-    }
     const int64_t m = L.m;
     const int r = L.r;
     const TcMap mp = L.tq;
@@ -738,14 +744,17 @@ __device__ void tcd_consumer(const Tables& t, const TcSeg* segs, int sb, int se,
   int stage = 0;
   uint32_t phase = 0;
   for (int si = sb; si < se; ++si) {
+    if (!t.layers[segs[si].layer].mat) {  // vectors: unpack from the parity's buffer
+      si = vector_run(t, segs, si, se, warp, kTcNW, [&](const TcSeg& s, const LayerDesc& L, int first, int stride) {
+             float* grad = t.grads[s.layer];
+             const float* slot = (MODE == 2 ? t.pbuf + L.p_off : t.qbuf + L.q_off);
+             for (int64_t i = s.row0 + first; i < s.row1; i += stride) grad[i] = slot[i] * scale;
+           }) - 1;
+      continue;
+    }
     const TcSeg s = segs[si];
     const LayerDesc& L = t.layers[s.layer];
     float* grad = t.grads[s.layer];
-    if (!L.mat) {  // vector: unpack from the parity's buffer
-      const float* slot = (MODE == 2 ? t.pbuf + L.p_off : t.qbuf + L.q_off);
-      for (int64_t i = s.row0 + threadIdx.x; i < s.row1; i += kTcNW * 32) grad[i] = slot[i] * scale;
-      continue;
-    }
     const int64_t m = L.m, n = L.n;
     const int r = L.r;
     const bool v4 = (m % 4 == 0) && ((reinterpret_cast<uintptr_t>(grad) & 15u) == 0);
@@ -851,6 +860,7 @@ tc_kernel(Tables t, const TcSeg* __restrict__ segs, const int32_t* __restrict__ 
   }
   __syncthreads();
   const int sb = cta_begin[blockIdx.x], se = cta_begin[blockIdx.x + 1];
+  prefetch_segs(t, segs, sb, se);
   const bool producer = (threadIdx.x >> 5) == kTcNW;
   if constexpr (MODE == 0) {
     if (producer) tcp_producer<R8>(t, segs, sb, se, sh);
