@@ -149,6 +149,8 @@ struct Tables {
   double* gram;
   double* wmat;
   int32_t* orthcnt;
+  long long* orthflag;   // K2: per layer, epoch of the phase that may start (step * 4 + phase)
+  int32_t* orthwork;     // K2 persistent queue: [0] next item, [1] exited CTAs
   uint32_t* degmask;
   int64_t* step;         // device step counter (keys the method's random draws)
   int32_t* deferred;     // 1: E holds S = M' of the last Q-step (E = S - P Q_loc^T

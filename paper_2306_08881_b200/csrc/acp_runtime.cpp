@@ -89,6 +89,7 @@ struct Plan {
   // workspace byte offsets
   size_t off_E = 0, off_P = 0, off_Q = 0, off_QL = 0, off_colpart = 0, off_colcnt = 0,
          off_gram = 0, off_wmat = 0, off_orthcnt = 0, off_degmask = 0, off_layers = 0,
+         off_orthflag = 0, off_orthwork = 0,
          off_grads = 0, off_rowsegs = 0, off_colsegs = 0, off_streamsegs = 0, off_orth[2] = {0, 0},
          off_ctab = 0, off_step = 0, off_red = 0, off_defer = 0,
          off_qsplit = 0, off_qlsplit = 0, off_psplit = 0, off_plsplit = 0, off_tcsegs = 0,
@@ -677,6 +678,8 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
   P.off_gram = take(8 * (size_t)P.gram_elems);
   P.off_wmat = take(8 * (size_t)P.wmat_elems);
   P.off_orthcnt = take(4 * (size_t)P.T);
+  P.off_orthflag = take(8 * (size_t)P.T);
+  P.off_orthwork = take(8);
   P.off_degmask = take(4 * (size_t)P.T);
   P.off_layers = take(sizeof(LayerDesc) * P.L.size());
   P.off_grads = take(8 * (size_t)P.T);
@@ -972,6 +975,8 @@ acp_status acp_create(const acp_config* cfg, acp_ctx** out) {
   t.gram = reinterpret_cast<double*>(c->ws + P.off_gram);
   t.wmat = reinterpret_cast<double*>(c->ws + P.off_wmat);
   t.orthcnt = reinterpret_cast<int32_t*>(c->ws + P.off_orthcnt);
+  t.orthflag = reinterpret_cast<long long*>(c->ws + P.off_orthflag);
+  t.orthwork = reinterpret_cast<int32_t*>(c->ws + P.off_orthwork);
   t.degmask = reinterpret_cast<uint32_t*>(c->ws + P.off_degmask);
   t.step = reinterpret_cast<int64_t*>(c->ws + P.off_step);
   t.deferred = reinterpret_cast<int32_t*>(c->ws + P.off_defer);

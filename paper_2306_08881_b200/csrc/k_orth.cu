@@ -13,6 +13,8 @@
 // sweep, so a 30522 x 32 factor is spread over 120 CTAs instead of serialising
 // 2r dependent reductions on one SM. The Gram partials are summed in a fixed
 // order (deterministic: every rank computes bit-identical factors).
+#include <algorithm>
+
 #include "k_common.cuh"
 
 namespace acp {
@@ -27,11 +29,16 @@ constexpr size_t orth_smem() {
   return (size_t)2 * RT * kLd * 4 + (size_t)3 * RT * RT * 8 + kThreads * 8 + 16;
 }
 
+// Layer `s.layer`'s phase `phase` may start once lflag[layer] >= ready_epoch
+// (set by the layer's last segment of the previous phase).
+__device__ __forceinline__ long long orth_epoch(int64_t step, int phase) { return step * 4 + phase; }
+
+// One (phase, segment) work item of K2. Returns after the item; the layer's
+// last segment of phases 0 / 1 also computes W1 / W2 and publishes the
+// layer's next phase through lflag.
 template <int RT>
-__global__ void __launch_bounds__(kThreads) orth_kernel(Tables t, int side,
-                                                        const OrthSeg* __restrict__ segs,
-                                                        int phase, uint64_t seed) {
-  extern __shared__ __align__(16) unsigned char orth_smem_raw[];
+__device__ void orth_item(const Tables& t, int side, const OrthSeg& s, int phase, uint64_t seed,
+                          int64_t step, unsigned char* orth_smem_raw) {
   float* A = reinterpret_cast<float*>(orth_smem_raw);  // [RT][kLd] input rows (fp32)
   float* B = A + RT * kLd;                               // [RT][kLd] phase-1 output rows
   double* Wm = reinterpret_cast<double*>(B + RT * kLd);  // [RT*RT]
@@ -40,7 +47,6 @@ __global__ void __launch_bounds__(kThreads) orth_kernel(Tables t, int side,
   double* gred = Rm + RT * RT;                            // [kThreads]
   int* flag = reinterpret_cast<int*>(gred + kThreads);
 
-  const OrthSeg s = segs[blockIdx.x];
   const LayerDesc L = t.layers[s.layer];
   const int r = L.r;
   const int64_t len = side == 0 ? L.m : L.n;
@@ -49,10 +55,14 @@ __global__ void __launch_bounds__(kThreads) orth_kernel(Tables t, int side,
   double* W2 = W1 + r * r;
   const int tid = threadIdx.x;
   const int nr = (int)(s.row1 - s.row0);
-  const int64_t step = *t.step;
-  if (phase == 2 && blockIdx.x == 0 && tid == 0) {
-    // every CTA of phases 0-1 has read the step (stream order): advance it
-    *t.step = step + 1;
+  if (phase > 0) {  // wait for the layer's previous phase (W1 / W2 published)
+    if (tid == 0) {
+      volatile long long* f = t.orthflag + L.deg_idx;
+      const long long want = orth_epoch(step, phase);
+      while (*f < want) __nanosleep(64);
+      __threadfence();
+    }
+    __syncthreads();
   }
 
   // stage the segment's rows (coalesced along rows, k-major source)
@@ -104,7 +114,10 @@ __global__ void __launch_bounds__(kThreads) orth_kernel(Tables t, int side,
       }
       B[l * kLd + i] = vf;
     }
-    if (phase == 2) return;
+    if (phase == 2) {
+      __syncthreads();  // smem reuse by the CTA's next item
+      return;
+    }
     __syncthreads();
     G = B;
   }
@@ -150,7 +163,9 @@ __global__ void __launch_bounds__(kThreads) orth_kernel(Tables t, int side,
     *flag = (old == s.nseg - 1);
   }
   __syncthreads();
-  if (!*flag) return;
+  const int last = *flag;
+  __syncthreads();  // *flag is rewritten by the CTA's next item
+  if (!last) return;
   __threadfence();
 
   // last segment of the layer: sum the partials in segment order
@@ -209,6 +224,44 @@ __global__ void __launch_bounds__(kThreads) orth_kernel(Tables t, int side,
     if (lane == 0) {
       if (phase == 0) t.degmask[L.deg_idx] = dmask;
       t.orthcnt[L.deg_idx] = 0;  // re-arm
+      __threadfence();
+      // publish: the layer's next phase may start
+      *reinterpret_cast<volatile long long*>(t.orthflag + L.deg_idx) = orth_epoch(step, phase + 1);
+    }
+  }
+  __syncthreads();
+}
+
+// K2 as one persistent launch: CTAs take (phase, segment) items from a queue
+// ordered by phase (all phase-0 items first), so an item only ever waits on
+// items dequeued before it (no deadlock) and a layer's phases follow each
+// other without a grid-wide barrier or a kernel boundary. The last CTA to
+// exit re-arms the queue and advances the step counter (every CTA read it).
+template <int RT>
+__global__ void __launch_bounds__(kThreads) orth_kernel(Tables t, int side,
+                                                        const OrthSeg* __restrict__ segs, int nseg,
+                                                        uint64_t seed) {
+  extern __shared__ __align__(16) unsigned char orth_smem_raw[];
+  __shared__ int item_sh;
+  const int64_t step = *t.step;
+  const int total = 3 * nseg;
+  int* work = t.orthwork;  // [0] next item, [1] exited CTAs
+  for (;;) {
+    if (threadIdx.x == 0) item_sh = atomicAdd(work, 1);
+    __syncthreads();
+    const int it = item_sh;
+    __syncthreads();
+    if (it >= total) break;
+    const int phase = it / nseg;
+    orth_item<RT>(t, side, segs[it - phase * nseg], phase, seed, step, orth_smem_raw);
+  }
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(work + 1, 1) == (int)gridDim.x - 1) {
+      work[0] = 0;
+      work[1] = 0;
+      *t.step = step + 1;
+      __threadfence();
     }
   }
 }
@@ -264,28 +317,31 @@ cudaError_t launch_orth(int rt, const Tables& t, int side, const OrthSeg* segs, 
                         uint64_t seed, int64_t step, cudaStream_t s, int* launches) {
   if (nseg <= 0) return cudaSuccess;
   (void)step;
-  auto go = [&](auto kern, size_t smem, int phase) -> cudaError_t {
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  auto go = [&](auto kern, size_t smem) -> cudaError_t {
     cudaError_t e = allow_max_smem(reinterpret_cast<const void*>(kern));
     if (e != cudaSuccess) return e;
-    kern<<<nseg, kThreads, smem, s>>>(t, side, segs, phase, seed);
-    return cudaSuccess;
+    int occ = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem);
+    // every CTA must be resident (items wait on each other): at most one wave
+    const int grid = std::max(1, std::min(3 * nseg, nsm * std::max(1, occ)));
+    kern<<<grid, kThreads, smem, s>>>(t, side, segs, nseg, seed);
+    return cudaGetLastError();
   };
-  for (int phase = 0; phase < 3; ++phase) {
-    cudaError_t e0;
-    switch (rt) {
-      case 1: e0 = go(orth_kernel<1>, orth_smem<1>(), phase); break;
-      case 2: e0 = go(orth_kernel<2>, orth_smem<2>(), phase); break;
-      case 4: e0 = go(orth_kernel<4>, orth_smem<4>(), phase); break;
-      case 8: e0 = go(orth_kernel<8>, orth_smem<8>(), phase); break;
-      case 16: e0 = go(orth_kernel<16>, orth_smem<16>(), phase); break;
-      case 32: e0 = go(orth_kernel<32>, orth_smem<32>(), phase); break;
-      default: return cudaErrorInvalidValue;
-    }
-    if (e0 != cudaSuccess) return e0;
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    if (launches) ++*launches;
+  cudaError_t e;
+  switch (rt) {
+    case 1: e = go(orth_kernel<1>, orth_smem<1>()); break;
+    case 2: e = go(orth_kernel<2>, orth_smem<2>()); break;
+    case 4: e = go(orth_kernel<4>, orth_smem<4>()); break;
+    case 8: e = go(orth_kernel<8>, orth_smem<8>()); break;
+    case 16: e = go(orth_kernel<16>, orth_smem<16>()); break;
+    case 32: e = go(orth_kernel<32>, orth_smem<32>()); break;
+    default: return cudaErrorInvalidValue;
   }
+  if (e != cudaSuccess) return e;
+  if (launches) ++*launches;
   return cudaSuccess;
 }
 

@@ -878,7 +878,12 @@ cudaError_t allow_max_smem(const void* kern) {
   std::lock_guard<std::mutex> lk(mu);
   for (auto& d : done)
     if (d.first == kern && d.second == dev) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  // the dynamic limit plus the kernel's static shared memory must fit 227 KB
+  cudaFuncAttributes fa{};
+  cudaError_t e = cudaFuncGetAttributes(&fa, kern);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           227 * 1024 - (int)fa.sharedSizeBytes);
   if (e == cudaSuccess) done.emplace_back(kern, dev);
   return e;
 }
