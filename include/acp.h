@@ -142,6 +142,29 @@ acp_status acp_compress(acp_ctx* ctx, int32_t parity, float* const* grads,
                         float** out_buffer, int64_t* out_count, void* cuda_stream);
 acp_status acp_decompress(acp_ctx* ctx, int32_t parity, float* const* grads, void* cuda_stream);
 
+/* Bucket-granular step for wait-free back-propagation (WFBP, P:236, P:262;
+ * SURVEY NEXT-2). The same step as acp_step, split so that each bucket's
+ * projection and all-reduce start as soon as the bucket's gradients exist:
+ *   acp_step_begin(ctx, parity, grads, s)   orthogonalise the reused factors
+ *                                           (they do not depend on this step's
+ *                                           gradients); grads as in acp_step,
+ *                                           the pointers must stay valid until
+ *                                           acp_step_end
+ *   acp_bucket_ready(ctx, b, s)             bucket b (of this parity, ready
+ *                                           order, acp_num_buckets) is complete:
+ *                                           project + pack its tensors on s and
+ *                                           (world_size > 1) all-reduce its
+ *                                           buffer range on the comm stream
+ *   acp_step_end(ctx, s)                    wait for every bucket's all-reduce,
+ *                                           decode all tensors into grads
+ * Every bucket must be made ready exactly once between begin and end, in any
+ * order. Eager launches (no CUDA graph). Errors: ACP_E_INVAL on a bucket
+ * index out of range / a bucket made ready twice / calls out of order
+ * (context not poisoned); CUDA / NCCL failures poison the context. */
+acp_status acp_step_begin(acp_ctx* ctx, int32_t parity, float* const* grads, void* cuda_stream);
+acp_status acp_bucket_ready(acp_ctx* ctx, int32_t bucket, void* cuda_stream);
+acp_status acp_step_end(acp_ctx* ctx, void* cuda_stream);
+
 /* State of matrix tensor i (tests, checkpoint/resume). Device pointers; any
  * may be NULL to skip. P: n_i x r_i row-major, Q: m_i x r_i row-major,
  * E: n_i x m_i row-major. Asynchronous on cuda_stream. */

@@ -22,7 +22,7 @@ EXPORTED = (
     "acp_workspace_bytes", "acp_create", "acp_step", "acp_compress", "acp_decompress",
     "acp_get_state", "acp_set_state", "acp_plan_info", "acp_num_buckets", "acp_bucket_range",
     "acp_profile_enable", "acp_profile_reset", "acp_profile_read", "acp_launch_count",
-    "acp_set_graphs",
+    "acp_set_graphs", "acp_step_begin", "acp_bucket_ready", "acp_step_end",
     "acp_destroy", "acp_last_error", "acp_abi_version", "acp_nccl_unique_id",
     "acp_nccl_comm_create", "acp_nccl_comm_destroy",
 )
@@ -79,6 +79,9 @@ def load() -> C.CDLL:
         "acp_bucket_range": [vp, i32, i32, C.POINTER(i64), C.POINTER(i64)],
         "acp_profile_enable": [vp, i32],
         "acp_set_graphs": [vp, i32],
+        "acp_step_begin": [vp, i32, fpp, vp],
+        "acp_bucket_ready": [vp, i32, vp],
+        "acp_step_end": [vp, vp],
         "acp_profile_reset": [vp],
         "acp_profile_read": [vp, i32, C.POINTER(C.c_double), C.POINTER(i64), C.POINTER(C.c_double)],
         "acp_launch_count": [vp, C.POINTER(i64)],

@@ -145,6 +145,22 @@ class AcpContext:
         L.check(self._lib.acp_step(self._ctx, int(parity), self._grad_ptrs(grads),
                                    C.c_void_p(_stream_handle(stream))))
 
+    # -- bucket-granular step (WFBP, acp_step_begin / acp_bucket_ready / acp_step_end)
+    def step_begin(self, grads, parity: int, stream=None) -> None:
+        """Open a step: orthogonalise the reused factors. The gradient tensors
+        must keep their storage until step_end."""
+        L.check(self._lib.acp_step_begin(self._ctx, int(parity), self._grad_ptrs(grads),
+                                         C.c_void_p(_stream_handle(stream))))
+
+    def bucket_ready(self, bucket: int, stream=None) -> None:
+        """All tensors of `bucket` (this parity's bucket, ready order) hold their
+        gradients: project + pack them and start the bucket's all-reduce."""
+        L.check(self._lib.acp_bucket_ready(self._ctx, int(bucket), C.c_void_p(_stream_handle(stream))))
+
+    def step_end(self, stream=None) -> None:
+        """Wait for every bucket's all-reduce and decode into the gradients."""
+        L.check(self._lib.acp_step_end(self._ctx, C.c_void_p(_stream_handle(stream))))
+
     def compress(self, grads, parity: int, stream=None):
         """Split API: returns the parity's fused buffer as a torch view."""
         import torch

@@ -83,6 +83,7 @@ struct Plan {
   // all-reduce (the paper's fusion rule), issued as an NCCL group per compute
   // group as soon as the group's projection has finished.
   std::vector<Launch> k1_g[2], k3_g[2];
+  std::vector<Launch> k1_b[2];  // WFBP API: one projection launch per bucket
   std::vector<std::pair<int, int>> groups[2];  // [first bucket, last bucket]
   double orth_bytes[2] = {0, 0};
   int64_t colpart_elems = 0, colcnt_n = 1, gram_elems = 1;
@@ -635,6 +636,9 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
       }
     }
   }
+  // per-bucket projections for the WFBP API (acp_bucket_ready)
+  for (int p = 0; p < 2; ++p)
+    for (const auto& bk : P.buckets[p]) P.k1_b[p].push_back(k1_launch(p, bk));
   P.colcnt_n = std::max<int64_t>(P.colcnt_n, P.T);
   if (smem_overflow) return fail(ACP_E_INVAL, "internal: stream kernel shared memory exceeds 227 KB");
   // K2 segments per side (0: Q factors, length m; 1: P factors, length n)
@@ -734,6 +738,10 @@ struct acp_ctx {
   int64_t step_count = 0;
   bool e_deferred = false;  // host mirror of *tab.deferred
   int tc_state = 0;         // TC path: 0 E = S, 1 E = S - P_orth Q_loc^T, 2 E = S - P_loc Q_orth^T
+  // WFBP API state: -1 idle, else the open step's parity; per-bucket flags
+  int wf_parity = -1;
+  std::vector<char> wf_done;
+  std::vector<cudaEvent_t> wf_ev;  // per bucket: all-reduce finished (comm stream)
   std::vector<CUtensorMap> tmaps;  // TC path: host copy of the per-layer TMA maps
   int64_t launches = 0;
   bool poisoned = false;
@@ -1213,6 +1221,80 @@ acp_status acp_step(acp_ctx* c, int32_t parity, float* const* grads, void* strea
   return ACP_OK;
 }
 
+acp_status acp_step_begin(acp_ctx* c, int32_t parity, float* const* grads, void* stream) {
+  acp_status st = check_ctx(c);
+  if (st != ACP_OK) return st;
+  if (parity != 0 && parity != 1) return fail(ACP_E_INVAL, "parity must be 0 or 1");
+  if (c->P.psgd) return fail(ACP_E_INVAL, "the bucket API runs ACP-SGD only (not ACP_POWERSGD)");
+  if (c->wf_parity >= 0) return fail(ACP_E_INVAL, "acp_step_begin: a step is already open");
+  if (c->cfg.world_size > 1 && !c->comm)
+    return fail(ACP_E_INVAL, "world_size > 1 needs an NCCL communicator");
+  DeviceGuard dg(c->cfg.device);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if ((st = set_grads(c, grads, s)) != ACP_OK) return st;
+  if ((st = before_k1(c, parity, s)) != ACP_OK) return st;
+  if ((st = run_orth(c, parity, s)) != ACP_OK) return st;
+  const size_t nb = c->P.buckets[parity].size();
+  c->wf_done.assign(nb, 0);
+  while (c->wf_ev.size() < 2 * nb) {
+    cudaEvent_t ev;
+    CK(c, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event create");
+    c->wf_ev.push_back(ev);
+  }
+  c->wf_parity = parity;
+  return ACP_OK;
+}
+
+acp_status acp_bucket_ready(acp_ctx* c, int32_t b, void* stream) {
+  acp_status st = check_ctx(c);
+  if (st != ACP_OK) return st;
+  const int parity = c->wf_parity;
+  if (parity < 0) return fail(ACP_E_INVAL, "acp_bucket_ready: no open step (acp_step_begin)");
+  const Plan& P = c->P;
+  if (b < 0 || b >= (int32_t)P.buckets[parity].size()) return fail(ACP_E_INVAL, "bucket index out of range");
+  if (c->wf_done[b]) return fail(ACP_E_INVAL, "bucket made ready twice");
+  DeviceGuard dg(c->cfg.device);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if ((st = run_k1(c, parity, P.k1_b[parity][b], s)) != ACP_OK) return st;
+  if (c->cfg.world_size > 1) {
+    cudaEvent_t k1done = c->wf_ev[2 * b], ardone = c->wf_ev[2 * b + 1];
+    CK(c, cudaEventRecord(k1done, s), "event record");
+    CK(c, cudaStreamWaitEvent(c->comm_stream, k1done, 0), "stream wait");
+    float* buf = parity == 0 ? c->tab.pbuf : c->tab.qbuf;
+    ProfRec* r = prof_begin(c, ACP_K_ALLREDUCE, 4.0 * P.bcnt[parity][b], c->comm_stream);
+    const ncclResult_t nr = ncclAllReduce(buf + P.boff[parity][b], buf + P.boff[parity][b],
+                                          (size_t)P.bcnt[parity][b], ncclFloat, ncclSum, c->comm,
+                                          c->comm_stream);
+    prof_end(r, c->comm_stream);
+    if (nr != ncclSuccess) {
+      c->poisoned = true;
+      return fail(ACP_E_NCCL, std::string("ncclAllReduce: ") + ncclGetErrorString(nr));
+    }
+    CK(c, cudaEventRecord(ardone, c->comm_stream), "event record");
+  }
+  c->wf_done[b] = 1;
+  return ACP_OK;
+}
+
+acp_status acp_step_end(acp_ctx* c, void* stream) {
+  acp_status st = check_ctx(c);
+  if (st != ACP_OK) return st;
+  const int parity = c->wf_parity;
+  if (parity < 0) return fail(ACP_E_INVAL, "acp_step_end: no open step");
+  for (size_t b = 0; b < c->wf_done.size(); ++b)
+    if (!c->wf_done[b]) return fail(ACP_E_INVAL, "acp_step_end: bucket " + std::to_string(b) + " not ready");
+  DeviceGuard dg(c->cfg.device);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (c->cfg.world_size > 1)
+    for (size_t b = 0; b < c->wf_done.size(); ++b)
+      CK(c, cudaStreamWaitEvent(s, c->wf_ev[2 * b + 1], 0), "stream wait");
+  if ((st = run_k3(c, parity, c->P.k3_all[parity], s)) != ACP_OK) return st;
+  after_k1(c, parity);
+  ++c->step_count;
+  c->wf_parity = -1;
+  return ACP_OK;
+}
+
 acp_status acp_set_graphs(acp_ctx* c, int32_t enable) {
   if (!c) return fail(ACP_E_INVAL, "ctx is NULL");
   c->use_graphs = enable != 0;
@@ -1367,6 +1449,7 @@ acp_status acp_destroy(acp_ctx* c) {
   }
   for (auto ev : c->ev_k1) cudaEventDestroy(ev);
   for (auto ev : c->ev_ar) cudaEventDestroy(ev);
+  for (auto ev : c->wf_ev) cudaEventDestroy(ev);
   for (auto& r : c->prof) {
     cudaEventDestroy(r.a);
     cudaEventDestroy(r.b);

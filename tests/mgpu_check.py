@@ -46,7 +46,14 @@ def main():
         o = oc(shapes, rank_r, world_size=world, seed=seed, q0=q0)
         for t in range(steps):
             g = [torch.from_numpy(np.ascontiguousarray(x)).cuda() for x in inputs[t][rank]]
-            ctx.step(g, t % 2)
+            if bucket_bytes == 0 and not flags:
+                # the bucket-granular (WFBP) API, buckets made ready in reverse order
+                ctx.step_begin(g, t % 2)
+                for b in reversed(range(len(ctx.buckets(t % 2)))):
+                    ctx.bucket_ready(b)
+                ctx.step_end()
+            else:
+                ctx.step(g, t % 2)
             ref = o.step(inputs[t], t % 2)
             torch.cuda.synchronize()
             for i, (a, b) in enumerate(zip(g, ref)):
