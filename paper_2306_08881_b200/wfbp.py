@@ -62,6 +62,8 @@ class Wfbp:
             p.grad.zero_()
         self.parity = parity
         self.left = list(self.size[parity])
+        if not self.overlap:
+            return  # naive: one whole acp_step after the backward pass
         self.ctx.step_begin(self.grads, parity)
         if self.side is not None:
             self.side.wait_stream(torch.cuda.current_stream())
@@ -88,9 +90,10 @@ class Wfbp:
         for the all-reduces and decode into p.grad."""
         import torch
         if not self.overlap:
-            for b in range(len(self.left)):
-                self._ready(b)
-        elif any(self.left):
+            self.ctx.step(self.grads, self.parity)  # the whole step (CUDA graph)
+            self.parity = None
+            return
+        if any(self.left):
             raise RuntimeError(f"buckets without gradients: {[b for b, n in enumerate(self.left) if n]}")
         if self.side is not None:
             torch.cuda.current_stream().wait_stream(self.side)
