@@ -248,6 +248,9 @@ def _measure(model, r, world, rank, local, args, comm, profile=True, flags=0):
         grads.append((g / (m ** 0.5)).contiguous())
     ctx = AcpContext(shapes, r, world_size=world, nccl_comm=comm, seed=7,
                      bucket_bytes=args.bucket_bytes, flags=flags)
+    nvls = False
+    if world > 1 and args.allreduce == "nvls" and not flags:
+        nvls = ctx.attach_symmetric()  # False when the box has no multicast
     ctx.set_graphs(not args.no_graphs)
     stream = torch.cuda.current_stream()
     for t in range(args.warmup):
@@ -290,7 +293,8 @@ def _measure(model, r, world, rank, local, args, comm, profile=True, flags=0):
         ctx.profile(False)
     nb = (len(ctx.buckets(0)), len(ctx.buckets(1)))
     return {"ctx": ctx, "grads": grads, "shapes": shapes, "nel": nel, "ms": ms, "prof": prof,
-            "launches": launches, "clocks": clk.summary(), "buckets": nb, "step_stats": step_stats}
+            "launches": launches, "clocks": clk.summary(), "buckets": nb, "step_stats": step_stats,
+            "allreduce": ("nvls" if nvls else "nccl") if world > 1 else None}
 
 
 def _ssgd(nel, world, args):
@@ -454,7 +458,7 @@ def run_ours(args):
                        "buckets_PQ": list(res["buckets"]) if world > 1 else [1, 1],
                        "bucket_rule": f"{args.bucket_bytes} B x compression rate (P:257)",
                        "l2": "inputs larger than L2 (M+E working set > 126 MB), no flush",
-                       "parallelism": f"dp{world}"},
+                       "parallelism": f"dp{world}", "allreduce": res["allreduce"]},
             "step_hbm_frac_16B": 16.0 * nel / (ms * 1e-3) / 1e9 / peak,
             "step_stats": res["step_stats"],
             "nvlink": _nvlink(res["prof"], world),
@@ -489,6 +493,8 @@ def main(argv=None):
     ap.add_argument("--no-graphs", action="store_true")
     ap.add_argument("--no-powersgd", action="store_true",
                     help="skip the on-box Power-SGD comparison line")
+    ap.add_argument("--allreduce", default="nccl", choices=["nccl", "nvls"],
+                    help="N > 1: NCCL per bucket group, or the library's NVLS kernel (symmetric memory)")
     ap.add_argument("--no-ssgd", action="store_true",
                     help="skip the dense S-SGD all-reduce comparison (N > 1)")
     ap.add_argument("--oracle-every", type=int, default=3)

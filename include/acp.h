@@ -165,6 +165,23 @@ acp_status acp_step_begin(acp_ctx* ctx, int32_t parity, float* const* grads, voi
 acp_status acp_bucket_ready(acp_ctx* ctx, int32_t bucket, void* cuda_stream);
 acp_status acp_step_end(acp_ctx* ctx, void* cuda_stream);
 
+/* NVLS all-reduce (world_size > 1, NVSwitch systems with
+ * multicast). The caller allocates a symmetric buffer of
+ * acp_symmetric_bytes() bytes on every rank (same size, bound to one
+ * NVLink-SHARP multicast object, e.g. torch symmetric memory) and passes this
+ * rank's unicast address, the multicast address, every rank's unicast
+ * address as mapped on this device (peers[world_size], index = rank in the
+ * symmetric group) and this rank's index. The context moves its fused P / Q
+ * buffers into the region and from then on all-reduces each compute group
+ * (acp_step) or bucket (acp_bucket_ready) with its own kernel: in-switch
+ * reduction (multimem.ld_reduce) + multicast store, instead of NCCL.
+ * Collective: every rank calls it, then the caller barriers before the next
+ * step. Synchronous. ACP_E_INVAL: world_size == 1, too small a region,
+ * world_size > 8. */
+acp_status acp_symmetric_bytes(acp_ctx* ctx, int64_t* out_bytes);
+acp_status acp_attach_symmetric(acp_ctx* ctx, void* local, void* multicast, void* const* peers,
+                                int32_t rank, int64_t bytes);
+
 /* State of matrix tensor i (tests, checkpoint/resume). Device pointers; any
  * may be NULL to skip. P: n_i x r_i row-major, Q: m_i x r_i row-major,
  * E: n_i x m_i row-major. Asynchronous on cuda_stream. */

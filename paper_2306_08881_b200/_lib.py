@@ -23,6 +23,7 @@ EXPORTED = (
     "acp_get_state", "acp_set_state", "acp_plan_info", "acp_num_buckets", "acp_bucket_range",
     "acp_profile_enable", "acp_profile_reset", "acp_profile_read", "acp_launch_count",
     "acp_set_graphs", "acp_step_begin", "acp_bucket_ready", "acp_step_end",
+    "acp_symmetric_bytes", "acp_attach_symmetric",
     "acp_destroy", "acp_last_error", "acp_abi_version", "acp_nccl_unique_id",
     "acp_nccl_comm_create", "acp_nccl_comm_destroy",
 )
@@ -82,6 +83,8 @@ def load() -> C.CDLL:
         "acp_step_begin": [vp, i32, fpp, vp],
         "acp_bucket_ready": [vp, i32, vp],
         "acp_step_end": [vp, vp],
+        "acp_symmetric_bytes": [vp, C.POINTER(i64)],
+        "acp_attach_symmetric": [vp, vp, vp, fpp, i32, i64],
         "acp_profile_reset": [vp],
         "acp_profile_read": [vp, i32, C.POINTER(C.c_double), C.POINTER(i64), C.POINTER(C.c_double)],
         "acp_launch_count": [vp, C.POINTER(i64)],

@@ -145,6 +145,35 @@ class AcpContext:
         L.check(self._lib.acp_step(self._ctx, int(parity), self._grad_ptrs(grads),
                                    C.c_void_p(_stream_handle(stream))))
 
+    # -- NVLS all-reduce (acp_attach_symmetric) ------------------------------
+    def attach_symmetric(self, group=None) -> bool:
+        """Move the fused buffers into torch symmetric memory bound to an NVLS
+        multicast object and all-reduce with the library's in-switch kernel
+        instead of NCCL (collective over `group`). Returns False (nothing
+        changed) when the device has no multicast support."""
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+        if group is None:
+            group = dist.group.WORLD
+        need = C.c_int64()
+        L.check(self._lib.acp_symmetric_bytes(self._ctx, C.byref(need)))
+        buf = symm_mem.empty(int(need.value), dtype=torch.uint8, device=self.device)
+        h = symm_mem.rendezvous(buf, group.group_name)
+        ok = torch.tensor([1 if h.multicast_ptr else 0], device=self.device)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+        if not int(ok.item()):
+            return False
+        peers = (C.c_void_p * h.world_size)(*h.buffer_ptrs)
+        L.check(self._lib.acp_attach_symmetric(self._ctx, C.c_void_p(buf.data_ptr()),
+                                               C.c_void_p(h.multicast_ptr),
+                                               C.cast(peers, C.POINTER(C.c_void_p)),
+                                               int(h.rank), int(need.value)))
+        torch.cuda.synchronize()
+        dist.barrier(group=group)
+        self._symm = (buf, h)  # keep the region alive with the context
+        return True
+
     # -- bucket-granular step (WFBP, acp_step_begin / acp_bucket_ready / acp_step_end)
     def step_begin(self, grads, parity: int, stream=None) -> None:
         """Open a step: orthogonalise the reused factors. The gradient tensors

@@ -166,6 +166,20 @@ struct Tables {
                              // boxes), [M, S] (Q-step boxes of tq.tr rows), [Q slot]: 9 maps
 };
 
+// NVLS all-reduce (k_nvls.cu): the fused buffers live in a
+// symmetric region bound to a multicast object; flags for the cross-rank
+// barriers sit behind the buffers in the same region.
+constexpr int kNvlsMaxCtas = 64, kNvlsMaxRanks = 8;
+struct NvlsArgs {
+  float* mc;                              // multicast address of the buffer being reduced
+  uint32_t* my_flags;                     // this rank's flag region
+  uint32_t* peer_flags[kNvlsMaxRanks];    // every rank's flag region, as mapped here
+  uint32_t* epoch;                        // [kNvlsMaxCtas] per-CTA launch counters (local)
+  int32_t rank, world;
+};
+// sum over ranks of floats [off, off + cnt) of the buffer behind a.mc (16-byte aligned)
+cudaError_t launch_nvls_allreduce(const NvlsArgs& a, int64_t off, int64_t cnt, cudaStream_t s);
+
 // launches (all on `stream`, 256 threads, grid = ncta)
 // mode 0: K1 P-step (projection + residual + pack into P-buffer)
 // mode 1: K3 P-step decode (+ unpack from P-buffer)

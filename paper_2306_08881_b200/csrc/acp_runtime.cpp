@@ -742,6 +742,12 @@ struct acp_ctx {
   int wf_parity = -1;
   std::vector<char> wf_done;
   std::vector<cudaEvent_t> wf_ev;  // per bucket: all-reduce finished (comm stream)
+  // NVLS all-reduce (acp_attach_symmetric)
+  bool nvls = false;
+  NvlsArgs nv{};
+  float* mc_base = nullptr;
+  int64_t sym_q_off = 0;           // floats: Q buffer inside the symmetric region
+  uint32_t* nvls_epoch = nullptr;  // device, kNvlsMaxCtas counters
   std::vector<CUtensorMap> tmaps;  // TC path: host copy of the per-layer TMA maps
   int64_t launches = 0;
   bool poisoned = false;
@@ -1100,6 +1106,26 @@ void after_k1(acp_ctx* c, int32_t parity) {
   if (c->P.tc) c->tc_state = parity == 0 ? 2 : 1;
 }
 
+// All-reduce floats [off, off + cnt) of the parity's fused buffer on the comm
+// stream: the NVLS kernel when a symmetric region is attached, else NCCL.
+acp_status allreduce_range(acp_ctx* c, int parity, int64_t off, int64_t cnt) {
+  float* buf = parity == 0 ? c->tab.pbuf : c->tab.qbuf;
+  if (c->nvls) {
+    NvlsArgs a = c->nv;
+    a.mc = c->mc_base + (parity == 0 ? 0 : c->sym_q_off);
+    CK(c, launch_nvls_allreduce(a, off, cnt, c->comm_stream), "NVLS all-reduce");
+    ++c->launches;
+    return ACP_OK;
+  }
+  const ncclResult_t nr = ncclAllReduce(buf + off, buf + off, (size_t)cnt, ncclFloat, ncclSum, c->comm,
+                                        c->comm_stream);
+  if (nr != ncclSuccess) {
+    c->poisoned = true;
+    return fail(ACP_E_NCCL, std::string("ncclAllReduce: ") + ncclGetErrorString(nr));
+  }
+  return ACP_OK;
+}
+
 // Per compute group: projection K1 of `parity` on s, then the group's buckets
 // all-reduced as one NCCL group on the comm stream (event ev_ar[g] marks it).
 acp_status project_and_reduce(acp_ctx* c, int32_t parity, cudaStream_t s) {
@@ -1115,17 +1141,25 @@ acp_status project_and_reduce(acp_ctx* c, int32_t parity, cudaStream_t s) {
     double bytes = 0;
     for (int b = b0; b <= b1; ++b) bytes += 4.0 * P.bcnt[parity][b];
     ProfRec* r = prof_begin(c, ACP_K_ALLREDUCE, bytes, c->comm_stream);
-    ncclResult_t nr = ncclGroupStart();
-    for (int b = b0; b <= b1 && nr == ncclSuccess; ++b)
-      nr = ncclAllReduce(buf + P.boff[parity][b], buf + P.boff[parity][b],
-                         (size_t)P.bcnt[parity][b], ncclFloat, ncclSum, c->comm, c->comm_stream);
-    const ncclResult_t ne = ncclGroupEnd();
-    if (nr == ncclSuccess) nr = ne;
-    prof_end(r, c->comm_stream);
-    if (nr != ncclSuccess) {
-      c->poisoned = true;
-      return fail(ACP_E_NCCL, std::string("ncclAllReduce: ") + ncclGetErrorString(nr));
+    if (c->nvls) {
+      // the group's buckets are one contiguous range of the buffer
+      const int64_t off = P.boff[parity][b0];
+      const int64_t end = P.boff[parity][b1] + P.bcnt[parity][b1];
+      if ((st = allreduce_range(c, parity, off, end - off)) != ACP_OK) return st;
+    } else {
+      ncclResult_t nr = ncclGroupStart();
+      for (int b = b0; b <= b1 && nr == ncclSuccess; ++b)
+        nr = ncclAllReduce(buf + P.boff[parity][b], buf + P.boff[parity][b],
+                           (size_t)P.bcnt[parity][b], ncclFloat, ncclSum, c->comm, c->comm_stream);
+      const ncclResult_t ne = ncclGroupEnd();
+      if (nr == ncclSuccess) nr = ne;
+      if (nr != ncclSuccess) {
+        prof_end(r, c->comm_stream);
+        c->poisoned = true;
+        return fail(ACP_E_NCCL, std::string("ncclAllReduce: ") + ncclGetErrorString(nr));
+      }
     }
+    prof_end(r, c->comm_stream);
     CK(c, cudaEventRecord(c->ev_ar[g], c->comm_stream), "event record");
   }
   return ACP_OK;
@@ -1260,16 +1294,10 @@ acp_status acp_bucket_ready(acp_ctx* c, int32_t b, void* stream) {
     cudaEvent_t k1done = c->wf_ev[2 * b], ardone = c->wf_ev[2 * b + 1];
     CK(c, cudaEventRecord(k1done, s), "event record");
     CK(c, cudaStreamWaitEvent(c->comm_stream, k1done, 0), "stream wait");
-    float* buf = parity == 0 ? c->tab.pbuf : c->tab.qbuf;
     ProfRec* r = prof_begin(c, ACP_K_ALLREDUCE, 4.0 * P.bcnt[parity][b], c->comm_stream);
-    const ncclResult_t nr = ncclAllReduce(buf + P.boff[parity][b], buf + P.boff[parity][b],
-                                          (size_t)P.bcnt[parity][b], ncclFloat, ncclSum, c->comm,
-                                          c->comm_stream);
+    st = allreduce_range(c, parity, P.boff[parity][b], P.bcnt[parity][b]);
     prof_end(r, c->comm_stream);
-    if (nr != ncclSuccess) {
-      c->poisoned = true;
-      return fail(ACP_E_NCCL, std::string("ncclAllReduce: ") + ncclGetErrorString(nr));
-    }
+    if (st != ACP_OK) return st;
     CK(c, cudaEventRecord(ardone, c->comm_stream), "event record");
   }
   c->wf_done[b] = 1;
@@ -1292,6 +1320,65 @@ acp_status acp_step_end(acp_ctx* c, void* stream) {
   after_k1(c, parity);
   ++c->step_count;
   c->wf_parity = -1;
+  return ACP_OK;
+}
+
+static int64_t sym_layout(const Plan& P, int64_t* q_off, int64_t* flag_off) {
+  const int64_t qo = (P.arena[0] + 63) / 64 * 64;                 // floats, 256-byte aligned
+  const int64_t fo = ((qo + P.arena[1]) * 4 + 255) / 256 * 256;   // bytes
+  if (q_off) *q_off = qo;
+  if (flag_off) *flag_off = fo;
+  return fo + 2LL * kNvlsMaxCtas * kNvlsMaxRanks * 4;
+}
+
+acp_status acp_symmetric_bytes(acp_ctx* c, int64_t* out) {
+  if (!c || !out) return fail(ACP_E_INVAL, "bad arguments");
+  *out = sym_layout(c->P, nullptr, nullptr);
+  return ACP_OK;
+}
+
+acp_status acp_attach_symmetric(acp_ctx* c, void* local, void* multicast, void* const* peers,
+                                int32_t rank, int64_t bytes) {
+  acp_status st = check_ctx(c);
+  if (st != ACP_OK) return st;
+  const int world = c->cfg.world_size;
+  if (world < 2 || world > kNvlsMaxRanks) return fail(ACP_E_INVAL, "NVLS needs 2 <= world_size <= 8");
+  if (!local || !multicast || !peers || rank < 0 || rank >= world)
+    return fail(ACP_E_INVAL, "bad symmetric buffer arguments");
+  int64_t qo = 0, fo = 0;
+  if (bytes < sym_layout(c->P, &qo, &fo)) return fail(ACP_E_INVAL, "symmetric region too small");
+  if (c->wf_parity >= 0) return fail(ACP_E_INVAL, "a bucket step is open");
+  DeviceGuard dg(c->cfg.device);
+  char* base = reinterpret_cast<char*>(local);
+  float* np = reinterpret_cast<float*>(base);
+  float* nq = np + qo;
+  CK(c, cudaDeviceSynchronize(), "attach sync");
+  CK(c, cudaMemcpy(np, c->tab.pbuf, 4 * (size_t)c->P.arena[0], cudaMemcpyDeviceToDevice), "move P buffer");
+  CK(c, cudaMemcpy(nq, c->tab.qbuf, 4 * (size_t)c->P.arena[1], cudaMemcpyDeviceToDevice), "move Q buffer");
+  CK(c, cudaMemset(base + fo, 0, 2 * kNvlsMaxCtas * kNvlsMaxRanks * 4), "zero flags");
+  if (!c->nvls_epoch) {
+    CK(c, cudaMalloc(&c->nvls_epoch, 4 * kNvlsMaxCtas), "epoch alloc");
+    CK(c, cudaMemset(c->nvls_epoch, 0, 4 * kNvlsMaxCtas), "epoch zero");
+  }
+  c->tab.pbuf = np;
+  c->tab.qbuf = nq;
+  c->mc_base = reinterpret_cast<float*>(multicast);
+  c->sym_q_off = qo;
+  c->nv = NvlsArgs{};
+  c->nv.my_flags = reinterpret_cast<uint32_t*>(base + fo);
+  for (int p = 0; p < world; ++p)
+    c->nv.peer_flags[p] = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(peers[p]) + fo);
+  c->nv.epoch = c->nvls_epoch;
+  c->nv.rank = rank;
+  c->nv.world = world;
+  c->nvls = true;
+  // captured graphs and TMA maps hold the old buffer addresses
+  for (int p = 0; p < 2; ++p)
+    if (c->gexec[p]) {
+      cudaGraphExecDestroy(c->gexec[p]);
+      c->gexec[p] = nullptr;
+    }
+  std::fill(c->grads_cache.begin(), c->grads_cache.end(), nullptr);
   return ACP_OK;
 }
 
@@ -1450,6 +1537,7 @@ acp_status acp_destroy(acp_ctx* c) {
   for (auto ev : c->ev_k1) cudaEventDestroy(ev);
   for (auto ev : c->ev_ar) cudaEventDestroy(ev);
   for (auto ev : c->wf_ev) cudaEventDestroy(ev);
+  if (c->nvls_epoch) cudaFree(c->nvls_epoch);
   for (auto& r : c->prof) {
     cudaEventDestroy(r.a);
     cudaEventDestroy(r.b);

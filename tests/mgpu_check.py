@@ -38,11 +38,22 @@ def main():
     inputs = make_inputs(shapes, world, steps, seed, "lowrank")
     q0 = make_q0(shapes, rank_r, seed)
     worst = 0.0
-    # paper rule, one tensor per bucket, one bucket; then the Power-SGD baseline
-    for bucket_bytes, flags in ((25 * 2 ** 20, 0), (0, 0), (-1, 0), (25 * 2 ** 20, ACP_POWERSGD)):
+    # paper rule, one tensor per bucket, one bucket; the Power-SGD baseline;
+    # then the NVLS all-reduce (symmetric memory) with the paper rule and the
+    # bucket API
+    runs = [(25 * 2 ** 20, 0, False), (0, 0, False), (-1, 0, False), (25 * 2 ** 20, ACP_POWERSGD, False),
+            (25 * 2 ** 20, 0, True), (0, 0, True)]
+    for bucket_bytes, flags, nvls in runs:
         ctx = AcpContext(shapes, rank_r, world_size=world, nccl_comm=comm, seed=seed, q0=q0,
                          bucket_bytes=bucket_bytes, flags=flags)
+        if nvls and not ctx.attach_symmetric():
+            if rank == 0:
+                print("NVLS multicast unavailable: skipped")
+            ctx.close()
+            continue
         oc = PowerSgdOracle if flags else AcpOracle
+        if rank == 0:
+            print(f"run bucket_bytes={bucket_bytes} flags={flags} nvls={nvls}", flush=True)
         o = oc(shapes, rank_r, world_size=world, seed=seed, q0=q0)
         for t in range(steps):
             g = [torch.from_numpy(np.ascontiguousarray(x)).cuda() for x in inputs[t][rank]]
