@@ -250,7 +250,10 @@ def _measure(model, r, world, rank, local, args, comm, profile=True, flags=0):
                      bucket_bytes=args.bucket_bytes, flags=flags)
     nvls = False
     if world > 1 and args.allreduce == "nvls" and not flags:
-        nvls = ctx.attach_symmetric()  # False when the box has no multicast
+        try:
+            nvls = ctx.attach_symmetric()  # False when the box has no multicast
+        except Exception as e:  # no symmetric memory here: NCCL all-reduce
+            print(f"NVLS unavailable ({e}); using NCCL", file=sys.stderr)
     ctx.set_graphs(not args.no_graphs)
     stream = torch.cuda.current_stream()
     for t in range(args.warmup):
@@ -493,7 +496,7 @@ def main(argv=None):
     ap.add_argument("--no-graphs", action="store_true")
     ap.add_argument("--no-powersgd", action="store_true",
                     help="skip the on-box Power-SGD comparison line")
-    ap.add_argument("--allreduce", default="nccl", choices=["nccl", "nvls"],
+    ap.add_argument("--allreduce", default="nvls", choices=["nccl", "nvls"],
                     help="N > 1: NCCL per bucket group, or the library's NVLS kernel (symmetric memory)")
     ap.add_argument("--no-ssgd", action="store_true",
                     help="skip the dense S-SGD all-reduce comparison (N > 1)")

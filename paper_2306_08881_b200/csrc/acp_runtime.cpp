@@ -606,7 +606,9 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
     P.k3_all[p] = k3_launch(p, all);
   }
   if (cfg->world_size > 1) {
-    int ngroups = 2;  // measured on 2xB200 (BERT-L r=4): 1 grp 1.41 ms, 2 grp 1.40, 4 grp 1.44, 8 grp 1.61
+    // measured on 2xB200 after the load-balance work: 1 group 0.197 / 1.114 ms
+    // (ResNet-50 / BERT-L r=4), 2 groups 0.200 / 1.124, 4 groups 0.265 / 1.187
+    int ngroups = 1;
     if (const char* env = std::getenv("ACP_COMPUTE_GROUPS")) ngroups = std::max(1, std::atoi(env));
     for (int p = 0; p < 2; ++p) {
       // balance groups by gradient elements, cutting only at bucket boundaries
