@@ -496,7 +496,7 @@ def main(argv=None):
     ap.add_argument("--no-graphs", action="store_true")
     ap.add_argument("--no-powersgd", action="store_true",
                     help="skip the on-box Power-SGD comparison line")
-    ap.add_argument("--allreduce", default="nvls", choices=["nccl", "nvls"],
+    ap.add_argument("--allreduce", default="nccl", choices=["nccl", "nvls"],
                     help="N > 1: NCCL per bucket group, or the library's NVLS kernel (symmetric memory)")
     ap.add_argument("--no-ssgd", action="store_true",
                     help="skip the dense S-SGD all-reduce comparison (N > 1)")
