@@ -539,13 +539,15 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
     ln.cb_off = (int64_t)P.ctab.size();
     ln.stage_floats = std::max(4, mode == 0 ? tc_p_stage_floats(P.R8)
                                             : (mode == 1 ? tc_q_stage : tc_d_stage_floats(P.R8)));
+    // decodes run two CTAs per SM (more warps to hide the MMA chains)
+    const int tc_cps = mode >= 2 ? 2 : 1;
     ln.stages = (int)std::max<int64_t>(2, std::min<int64_t>(mode >= 2 ? 8 : 6,
-                                                            (200 * 1024) / (4LL * ln.stage_floats)));
+                                                            (200 * 1024 / tc_cps) / (4LL * ln.stage_floats)));
     if (tc_smem_bytes(ln.stages, ln.stage_floats) > 227 * 1024) smem_overflow = true;
     int64_t part = 0;
     int prev_layer = -1, prev_panel = -1;
     ln.red_off = (int64_t)P.redtasks.size();
-    ln.ncta = split_units(units, nsm, min_share, nsm, P.ctab, [&](const Unit& u, int64_t a, int64_t b) {
+    ln.ncta = split_units(units, nsm, min_share, nsm * tc_cps, P.ctab, [&](const Unit& u, int64_t a, int64_t b) {
       TcSeg sg{};
       sg.layer = u.layer;
       sg.row0 = a;

@@ -839,7 +839,7 @@ __device__ void tcd_consumer(const Tables& t, const TcSeg* segs, int sb, int se,
 }
 
 template <int MODE, int R8>
-__global__ void __launch_bounds__(kTcNW * 32 + 32, 1)
+__global__ void __launch_bounds__(kTcNW * 32 + 32, MODE >= 2 ? 2 : 1)
 tc_kernel(Tables t, const TcSeg* __restrict__ segs, const int32_t* __restrict__ cta_begin,
           int stages, int stage_floats, float scale) {
   extern __shared__ __align__(1024) unsigned char tc_smem_raw[];  // SWIZZLE_128B boxes
