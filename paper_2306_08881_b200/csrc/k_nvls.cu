@@ -25,6 +25,12 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
   return v;
 }
 
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 // flags: [2 barriers][kNvlsMaxCtas][kNvlsMaxRanks] uint32 per rank
 __device__ void cross_rank_barrier(const NvlsArgs& a, int which, uint32_t epoch) {
   const int slot = (which * kNvlsMaxCtas + blockIdx.x) * kNvlsMaxRanks;
@@ -32,7 +38,13 @@ __device__ void cross_rank_barrier(const NvlsArgs& a, int which, uint32_t epoch)
     const int p = threadIdx.x;
     __threadfence_system();
     st_release_sys(a.peer_flags[p] + slot + a.rank, epoch);
-    while ((int)(ld_acquire_sys(a.my_flags + slot + p) - epoch) < 0) __nanosleep(32);
+    // a peer that never arrives (crashed rank, mismatched launch sequence)
+    // must not hang the GPU: trap after 10 s, which fails the stream loudly
+    const uint64_t t0 = globaltimer_ns();
+    while ((int)(ld_acquire_sys(a.my_flags + slot + p) - epoch) < 0) {
+      __nanosleep(32);
+      if (globaltimer_ns() - t0 > 10000000000ull) __trap();
+    }
   }
   __syncthreads();
 }

@@ -541,30 +541,44 @@ __device__ void tcq_consumer(const Tables& t, const TcSeg* segs, int sb, int se,
       const float* fLl = fLh + tr * RS;
       const float* fPh = fLl + tr * RS;   // P_orth hi
       const float* fPl = fPh + tr * RS;
-      const bool full = (r0 + tr <= s.row1) && (mp.pc <= cols);
       float ta[CBW][KB][4];  // this tile's sums (short MMA chains, see the P-step)
 #pragma unroll
       for (int j = 0; j < CBW; ++j)
 #pragma unroll
         for (int kb = 0; kb < KB; ++kb) ta[j][kb][0] = ta[j][kb][1] = ta[j][kb][2] = ta[j][kb][3] = 0.f;
-      for (int ks = rg; ks < ksteps; ks += mp.wr) {
-        const int rowg = 8 * ks + g, rowa = 8 * ks + 2 * tq, rowb = rowa + 1;
+      // per-tile pointers: every shared load / store below is [pointer + constant]
+      const int ks0 = rg;  // this warp's first k-step (k-steps ks0, ks0 + wr, ...)
+      const float* pL = fLh + (8 * ks0 + g) * RS + tq;        // P_loc rows 8ks+g, ranks 8kb+t (+4)
+      const float* pLl = fLl + (8 * ks0 + g) * RS + tq;
+      const float* pP = fPh + (8 * ks0 + 2 * tq) * RS + g;    // P_orth rows 8ks+2t (+1), ranks 8kb+g
+      const float* pPl = fPl + (8 * ks0 + 2 * tq) * RS + g;
+      const float* xM[CBW][4];
+      float* xS[CBW][4];
+#pragma unroll
+      for (int j = 0; j < CBW; ++j) {
+        const int o[4] = {offa[j], offa1[j], offb[j], offb1[j]};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          xM[j][e] = sM + o[e] + 256 * ks0;
+          xS[j][e] = sS + o[e] + 256 * ks0;
+        }
+      }
+      auto kstep = [&](const int kk, const int ks) {  // kk: k-step index relative to ks0 (unrolled)
+        const int fo = 8 * RS * kk;  // kk = 1 only happens with wr = 1 (tr = 16)
+        const int xo = 256 * kk;
         // B fragments: P_loc (k = rank, n = row) and P_orth (k = row, n = rank)
         uint32_t lbh[KB][2], lbl[KB][2], pbh[KB][2], pbl[KB][2];
 #pragma unroll
         for (int kb = 0; kb < KB; ++kb) {
-          lbh[kb][0] = lds_u32(fLh + rowg * RS + 8 * kb + tq);
-          lbh[kb][1] = lds_u32(fLh + rowg * RS + 8 * kb + tq + 4);
-          lbl[kb][0] = lds_u32(fLl + rowg * RS + 8 * kb + tq);
-          lbl[kb][1] = lds_u32(fLl + rowg * RS + 8 * kb + tq + 4);
-          pbh[kb][0] = lds_u32(fPh + rowa * RS + 8 * kb + g);
-          pbh[kb][1] = lds_u32(fPh + rowb * RS + 8 * kb + g);
-          pbl[kb][0] = lds_u32(fPl + rowa * RS + 8 * kb + g);
-          pbl[kb][1] = lds_u32(fPl + rowb * RS + 8 * kb + g);
+          lbh[kb][0] = lds_u32(pL + fo + 8 * kb);
+          lbh[kb][1] = lds_u32(pL + fo + 8 * kb + 4);
+          lbl[kb][0] = lds_u32(pLl + fo + 8 * kb);
+          lbl[kb][1] = lds_u32(pLl + fo + 8 * kb + 4);
+          pbh[kb][0] = lds_u32(pP + fo + 8 * kb);
+          pbh[kb][1] = lds_u32(pP + fo + RS + 8 * kb);
+          pbl[kb][0] = lds_u32(pPl + fo + 8 * kb);
+          pbl[kb][1] = lds_u32(pPl + fo + RS + 8 * kb);
         }
-        const int ko = 256 * ks;  // 8 rows = 8 x 32 floats, same swizzle
-        float* Sa = S + (r0 + rowa) * m + c0;
-        float* Sb = Sa + m;
 #pragma unroll
         for (int j = 0; j < CBW; ++j) {
           if (!blk[j]) continue;
@@ -574,43 +588,40 @@ __device__ void tcq_consumer(const Tables& t, const TcSeg* segs, int sb, int se,
           for (int kb = 0; kb < KB; ++kb)
             mma3(c, ah[j][kb], al[j][kb], lbh[kb][0], lbh[kb][1], lbl[kb][0], lbl[kb][1]);
           // c0 (col g, row 2t), c1 (col g, row 2t+1), c2 (col g+8, row 2t), c3 (col g+8, row 2t+1)
-          const float x0 = sM[offa[j] + ko] + sS[offa[j] + ko] - c[0];
-          const float x1 = sM[offa1[j] + ko] + sS[offa1[j] + ko] - c[1];
-          const float x2 = sM[offb[j] + ko] + sS[offb[j] + ko] - c[2];
-          const float x3 = sM[offb1[j] + ko] + sS[offb1[j] + ko] - c[3];
-          const int ca = (cg * CBW + j) * 16 + g, cb2 = ca + 8;
+          float x[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) x[e] = xM[j][e][xo] + xS[j][e][xo] - c[e];
           if (tst) {  // back into the S tile; the tile is stored by TMA below
-            sS[offa[j] + ko] = x0;
-            sS[offa1[j] + ko] = x1;
-            sS[offb[j] + ko] = x2;
-            sS[offb1[j] + ko] = x3;
-          } else if (full) {
-            __stcs(Sa + ca, x0);
-            __stcs(Sb + ca, x1);
-            __stcs(Sa + cb2, x2);
-            __stcs(Sb + cb2, x3);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) xS[j][e][xo] = x[e];
           } else {
-            const bool va = r0 + rowa < s.row1, vb = r0 + rowb < s.row1;
+            const int rowa = 8 * ks + 2 * tq;
+            float* Sa = S + (r0 + rowa) * m + c0;
+            float* Sb = Sa + m;
+            const int ca = (cg * CBW + j) * 16 + g, cb2 = ca + 8;
+            const bool va = r0 + rowa < s.row1, vb = r0 + rowa + 1 < s.row1;
             if (ca < cols) {
-              if (va) __stcs(Sa + ca, x0);
-              if (vb) __stcs(Sb + ca, x1);
+              if (va) __stcs(Sa + ca, x[0]);
+              if (vb) __stcs(Sb + ca, x[1]);
             }
             if (cb2 < cols) {
-              if (va) __stcs(Sa + cb2, x2);
-              if (vb) __stcs(Sb + cb2, x3);
+              if (va) __stcs(Sa + cb2, x[2]);
+              if (vb) __stcs(Sb + cb2, x[3]);
             }
           }
           // projection Q += x^T P_orth: A = x^T (columns x rows), k t <-> row 2t
           uint32_t xh[4], xl[4];
-          split_tf32(x0, xh[0], xl[0]);
-          split_tf32(x2, xh[1], xl[1]);
-          split_tf32(x1, xh[2], xl[2]);
-          split_tf32(x3, xh[3], xl[3]);
+          split_tf32(x[0], xh[0], xl[0]);
+          split_tf32(x[2], xh[1], xl[1]);
+          split_tf32(x[1], xh[2], xl[2]);
+          split_tf32(x[3], xh[3], xl[3]);
 #pragma unroll
           for (int nb = 0; nb < KB; ++nb)
             mma3(ta[j][nb], xh, xl, pbh[nb][0], pbh[nb][1], pbl[nb][0], pbl[nb][1]);
         }
-      }
+      };
+      if (ks0 < ksteps) kstep(0, ks0);
+      if (ks0 + mp.wr < ksteps) kstep(1, ks0 + mp.wr);
 #pragma unroll
       for (int j = 0; j < CBW; ++j)
 #pragma unroll
