@@ -137,6 +137,9 @@ struct ColReduceTask {
   int32_t pad_;
 };
 
+struct NvlsArgs;
+struct FusedSync;
+
 struct Tables {
   const LayerDesc* layers;
   float* const* grads;   // device table of gradient pointers
@@ -162,7 +165,13 @@ struct Tables {
   float* psplit;         // P_orth  [2][n][R8] (written by K2, side 1)
   float* plsplit;        // P_loc   [2][n][R8] (written by the P-step TC kernel)
   int32_t r8;            // padded rank (multiple of 8), 0: TC path off
-  const CUtensorMap* tmaps;  // TC path: per layer [M, S, Q_orth hi, lo, Q_loc hi, lo] (P-step
+  const CUtensorMap* tmaps;
+  // NVLS all-reduce fused into the decode prologue (acp_attach_symmetric):
+  // nvls_fused != 0 -> the decode of parity p first sums buffer p over the
+  // ranks in the switch (k_nvls.cuh)
+  const NvlsArgs* nv;
+  FusedSync* fsync;
+  int32_t nvls_fused;  // TC path: per layer [M, S, Q_orth hi, lo, Q_loc hi, lo] (P-step
                              // boxes), [M, S] (Q-step boxes of tq.tr rows), [Q slot]: 9 maps
 };
 
@@ -176,9 +185,22 @@ struct NvlsArgs {
   uint32_t* peer_flags[kNvlsMaxRanks];    // every rank's flag region, as mapped here
   uint32_t* epoch;                        // [kNvlsMaxCtas] per-CTA launch counters (local)
   int32_t rank, world;
+  float* mc_buf[2];                       // multicast address of the P / Q buffer
+  int64_t n_buf[2];                       // floats of the P / Q buffer (multiple of 4)
 };
+// Fused all-reduce in the decode prologue: per parity, a grid arrival
+// counter, a release word and the launch epoch (monotonic, graph-safe).
+struct FusedSync {
+  uint32_t gcount, release, epoch, pad_;
+};
+// flag area: rows 0-1 separate all-reduce kernel, rows 2-5 fused prologue
+// (two per parity)
+constexpr int kNvlsFlagRows = 6;
 // sum over ranks of floats [off, off + cnt) of the buffer behind a.mc (16-byte aligned)
 cudaError_t launch_nvls_allreduce(const NvlsArgs& a, int64_t off, int64_t cnt, cudaStream_t s);
+// CTAs of a decode row kernel resident per SM (the fused prologue needs the
+// whole grid resident)
+int row_kernel_ctas_per_sm(int mode, int rt);
 
 // launches (all on `stream`, 256 threads, grid = ncta)
 // mode 0: K1 P-step (projection + residual + pack into P-buffer)

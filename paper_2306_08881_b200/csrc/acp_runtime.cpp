@@ -78,6 +78,7 @@ struct Plan {
   std::vector<OrthSeg> orthsegs[2];
   std::vector<int32_t> ctab;
   Launch k1_all[2], k3_all[2];
+  Launch k3_fused[2];  // decodes planned as one resident wave (NVLS-fused prologue)
   // world_size > 1: compute groups = runs of consecutive buckets whose
   // projection / decode run as one launch; each bucket is still its own
   // all-reduce (the paper's fusion rule), issued as an NCCL group per compute
@@ -94,7 +95,7 @@ struct Plan {
          off_grads = 0, off_rowsegs = 0, off_colsegs = 0, off_streamsegs = 0, off_orth[2] = {0, 0},
          off_ctab = 0, off_step = 0, off_red = 0, off_defer = 0,
          off_qsplit = 0, off_qlsplit = 0, off_psplit = 0, off_plsplit = 0, off_tcsegs = 0,
-         off_tmaps = 0,
+         off_tmaps = 0, off_nvargs = 0, off_fsync = 0,
          total = 0;
 };
 
@@ -292,7 +293,7 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
   const int max_grid = nsm * 8;
   const double min_share = 256.0 * 1024;
   const bool ef = P.ef;
-  auto row_launch = [&](int mode, const std::vector<int>& tensors) {
+  auto row_launch = [&](int mode, const std::vector<int>& tensors, bool one_wave = false) {
     std::vector<Unit> units;
     double bytes = 0;
     for (int i : tensors) {
@@ -319,7 +320,11 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
     ln.mode = mode;
     ln.seg_off = (int64_t)P.rowsegs.size();
     ln.cb_off = (int64_t)P.ctab.size();
-    ln.ncta = split_units(units, nsm, min_share, max_grid, P.ctab, [&](const Unit& u, int64_t a, int64_t b) {
+    // fused NVLS decodes: one resident wave, so the prologue can barrier the grid
+    const int grid_cap = (one_wave && (mode == 1 || mode == 2 || mode == 3))
+                             ? std::min(max_grid, nsm * std::max(1, row_kernel_ctas_per_sm(mode, P.RT)))
+                             : max_grid;
+    ln.ncta = split_units(units, nsm, min_share, grid_cap, P.ctab, [&](const Unit& u, int64_t a, int64_t b) {
       RowSeg s{};
       s.layer = u.layer;
       s.row0 = a;
@@ -607,6 +612,12 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
     P.k1_all[p] = k1_launch(p, all);
     P.k3_all[p] = k3_launch(p, all);
   }
+  if (cfg->world_size > 1) {  // decode variants for the NVLS-fused prologue
+    for (int p = 0; p < 2; ++p) {
+      if (P.tc) P.k3_fused[p] = P.k3_all[p];  // TC decodes are one wave already
+      else if (P.defer || !P.ef) P.k3_fused[p] = row_launch(p == 0 ? 1 : (P.defer ? 3 : 2), all, true);
+    }
+  }
   if (cfg->world_size > 1) {
     // measured on 2xB200 after the load-balance work: 1 group 0.197 / 1.114 ms
     // (ResNet-50 / BERT-L r=4), 2 groups 0.200 / 1.124, 4 groups 0.265 / 1.187
@@ -703,6 +714,8 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
   P.off_plsplit = take(4 * (size_t)P.ps_elems);
   P.off_tcsegs = take(sizeof(TcSeg) * P.tcsegs.size());
   P.off_tmaps = take(P.tc ? sizeof(CUtensorMap) * 9 * (size_t)P.T : 0);
+  P.off_nvargs = take(sizeof(NvlsArgs));
+  P.off_fsync = take(2 * sizeof(FusedSync));
   P.off_step = take(8);
   P.off_defer = take(8);
   P.off_red = take(sizeof(ColReduceTask) * P.redtasks.size());
@@ -752,6 +765,7 @@ struct acp_ctx {
   float* mc_base = nullptr;
   int64_t sym_q_off = 0;           // floats: Q buffer inside the symmetric region
   uint32_t* nvls_epoch = nullptr;  // device, kNvlsMaxCtas counters
+  bool nvls_fusable = false;       // acp_step: all-reduce inside the decode prologue
   std::vector<CUtensorMap> tmaps;  // TC path: host copy of the per-layer TMA maps
   int64_t launches = 0;
   bool poisoned = false;
@@ -852,19 +866,21 @@ acp_status run_k1(acp_ctx* c, int parity, const Launch& ln, cudaStream_t s) {
   return ACP_OK;
 }
 
-acp_status run_k3(acp_ctx* c, int parity, const Launch& ln, cudaStream_t s) {
+acp_status run_k3(acp_ctx* c, int parity, const Launch& ln, cudaStream_t s, bool fused = false) {
   if (ln.ncta <= 0) return ACP_OK;
   const int ef = c->P.ef ? 1 : 0;
+  Tables tt = c->tab;
+  tt.nvls_fused = fused ? 1 : 0;  // this decode first sums its buffer over the ranks (NVLS)
   ProfRec* r = prof_begin(c, parity == 0 ? ACP_K_DECODE_P : ACP_K_DECODE_Q, ln.bytes, s);
   cudaError_t e =
       ln.kind == 3
-          ? launch_tc(ln.mode, c->P.R8, c->tab, dev_tcsegs(c, ln), dev_ctab(c, ln), ln.ncta, ln.stages,
+          ? launch_tc(ln.mode, c->P.R8, tt, dev_tcsegs(c, ln), dev_ctab(c, ln), ln.ncta, ln.stages,
                       ln.stage_floats, decode_scale(c), s)
       : ln.kind == 2
-          ? launch_stream(ln.mode, c->P.RT, c->tab, dev_streamsegs(c, ln), dev_ctab(c, ln), ln.ncta,
+          ? launch_stream(ln.mode, c->P.RT, tt, dev_streamsegs(c, ln), dev_ctab(c, ln), ln.ncta,
                           decode_scale(c), ln.stages, ln.stage_floats, ln.factor_floats, ln.defer,
                           ln.ptile, s)
-          : launch_row(ln.mode, c->P.RT, c->tab, dev_rowsegs(c, ln), dev_ctab(c, ln),
+          : launch_row(ln.mode, c->P.RT, tt, dev_rowsegs(c, ln), dev_ctab(c, ln),
                        ln.ncta, decode_scale(c), ef, s);
   prof_end(r, s);
   if (e != cudaSuccess) return cuda_fail(c, e, "decode kernel launch");
@@ -1004,6 +1020,9 @@ acp_status acp_create(const acp_config* cfg, acp_ctx** out) {
   t.plsplit = reinterpret_cast<float*>(c->ws + P.off_plsplit);
   t.r8 = P.R8;
   t.tmaps = reinterpret_cast<const CUtensorMap*>(c->ws + P.off_tmaps);
+  t.nv = reinterpret_cast<const NvlsArgs*>(c->ws + P.off_nvargs);
+  t.fsync = reinterpret_cast<FusedSync*>(c->ws + P.off_fsync);
+  t.nvls_fused = 0;
 
   DeviceGuard dg(cfg->device);
   cudaStream_t s = nullptr;
@@ -1204,6 +1223,14 @@ acp_status enqueue_step(acp_ctx* c, int32_t parity, cudaStream_t s) {
     if ((st = run_k3(c, parity, P.k3_all[parity], s)) != ACP_OK) return st;
     return ACP_OK;
   }
+  if (c->nvls && c->nvls_fusable) {
+    // NEXT-3: one projection launch, then the decode sums the buffer over the
+    // ranks in the switch before decoding (no all-reduce launch, no comm stream)
+    if ((st = run_k1(c, parity, P.k1_all[parity], s)) != ACP_OK) return st;
+    ProfRec* r = prof_begin(c, ACP_K_ALLREDUCE, 0.0, s);  // marker only: fused into the decode
+    prof_end(r, s);
+    return run_k3(c, parity, P.k3_fused[parity], s, true);
+  }
   if ((st = project_and_reduce(c, parity, s)) != ACP_OK) return st;
   for (size_t g = 0; g < P.groups[parity].size(); ++g) {
     CK(c, cudaStreamWaitEvent(s, c->ev_ar[g], 0), "stream wait");
@@ -1332,7 +1359,7 @@ static int64_t sym_layout(const Plan& P, int64_t* q_off, int64_t* flag_off) {
   const int64_t fo = ((qo + P.arena[1]) * 4 + 255) / 256 * 256;   // bytes
   if (q_off) *q_off = qo;
   if (flag_off) *flag_off = fo;
-  return fo + 2LL * kNvlsMaxCtas * kNvlsMaxRanks * 4;
+  return fo + (int64_t)kNvlsFlagRows * kNvlsMaxCtas * kNvlsMaxRanks * 4;
 }
 
 acp_status acp_symmetric_bytes(acp_ctx* c, int64_t* out) {
@@ -1359,7 +1386,7 @@ acp_status acp_attach_symmetric(acp_ctx* c, void* local, void* multicast, void* 
   CK(c, cudaDeviceSynchronize(), "attach sync");
   CK(c, cudaMemcpy(np, c->tab.pbuf, 4 * (size_t)c->P.arena[0], cudaMemcpyDeviceToDevice), "move P buffer");
   CK(c, cudaMemcpy(nq, c->tab.qbuf, 4 * (size_t)c->P.arena[1], cudaMemcpyDeviceToDevice), "move Q buffer");
-  CK(c, cudaMemset(base + fo, 0, 2 * kNvlsMaxCtas * kNvlsMaxRanks * 4), "zero flags");
+  CK(c, cudaMemset(base + fo, 0, kNvlsFlagRows * kNvlsMaxCtas * kNvlsMaxRanks * 4), "zero flags");
   if (!c->nvls_epoch) {
     CK(c, cudaMalloc(&c->nvls_epoch, 4 * kNvlsMaxCtas), "epoch alloc");
     CK(c, cudaMemset(c->nvls_epoch, 0, 4 * kNvlsMaxCtas), "epoch zero");
@@ -1375,7 +1402,16 @@ acp_status acp_attach_symmetric(acp_ctx* c, void* local, void* multicast, void* 
   c->nv.epoch = c->nvls_epoch;
   c->nv.rank = rank;
   c->nv.world = world;
+  c->nv.mc_buf[0] = c->mc_base;
+  c->nv.mc_buf[1] = c->mc_base + qo;
+  c->nv.n_buf[0] = (c->P.arena[0] + 3) / 4 * 4;
+  c->nv.n_buf[1] = (c->P.arena[1] + 3) / 4 * 4;
+  CK(c, cudaMemcpy(c->ws + c->P.off_nvargs, &c->nv, sizeof(NvlsArgs), cudaMemcpyHostToDevice), "NVLS args");
+  CK(c, cudaMemset(c->ws + c->P.off_fsync, 0, 2 * sizeof(FusedSync)), "fused sync");
   c->nvls = true;
+  // the decode kernels (row / TC) sum the buffer in their prologue; the
+  // stream K3-Q (ACP_NO_DEFER) and Power-SGD keep the separate kernel
+  c->nvls_fusable = (!c->P.psgd && (c->P.tc || c->P.defer || !c->P.ef)) && !std::getenv("ACP_NVLS_UNFUSED");
   // captured graphs and TMA maps hold the old buffer addresses
   for (int p = 0; p < 2; ++p)
     if (c->gexec[p]) {

@@ -22,6 +22,7 @@
 // through L1 (__ldg) and reused by every row of the layer the CTA processes;
 // M and E use streaming (.cs) accesses so they do not evict it.
 #include "k_common.cuh"
+#include "k_nvls.cuh"
 
 namespace acp {
 namespace {
@@ -377,6 +378,8 @@ __global__ void __launch_bounds__(kThreads) row_kernel(Tables t, const RowSeg* _
   __shared__ __align__(16) float red[2 * 8 * kRedSlots];
   __shared__ __align__(16) float red_gen[8 * 32];
   int phase = 0;
+  // NVLS (NEXT-3): sum this parity's fused buffer over the ranks first
+  if (MODE != 0 && t.nvls_fused) nvls_fused_reduce(t, MODE == 1 ? 0 : 1);
   // the P-step decode runs after the P-step projection consumed a deferred
   // Q-step residual (k_stream.cu): E is materialised again
   if (MODE == 1 && blockIdx.x == 0 && threadIdx.x == 0) *t.deferred = 0;
@@ -440,6 +443,26 @@ cudaError_t launch_row_mode(int rt, const Tables& t, const RowSeg* segs, const i
 }
 
 }  // namespace
+
+int row_kernel_ctas_per_sm(int mode, int rt) {
+  int n = 1;
+  auto occ = [&](auto kern) { cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, kThreads, 0); };
+#define ACP_OCC(M)                                      \
+  switch (rt) {                                        \
+    case 1: occ(row_kernel<M, 1>); break;              \
+    case 2: occ(row_kernel<M, 2>); break;              \
+    case 4: occ(row_kernel<M, 4>); break;              \
+    case 8: occ(row_kernel<M, 8>); break;              \
+    case 16: occ(row_kernel<M, 16>); break;            \
+    default: occ(row_kernel<M, 32>); break;            \
+  }
+  if (mode == 1) { ACP_OCC(1) }
+  else if (mode == 2) { ACP_OCC(2) }
+  else if (mode == 3) { ACP_OCC(3) }
+  else { ACP_OCC(0) }
+#undef ACP_OCC
+  return n;
+}
 
 int row_rows_per_iter(int mode, int V, int rt) {
   if (mode == 0) return rows_k1p(V, rt);

@@ -30,6 +30,7 @@
 #include <cstring>
 
 #include "k_common.cuh"
+#include "k_nvls.cuh"
 
 namespace acp {
 namespace {
@@ -872,6 +873,9 @@ tc_kernel(Tables t, const TcSeg* __restrict__ segs, const int32_t* __restrict__ 
   __syncthreads();
   const int sb = cta_begin[blockIdx.x], se = cta_begin[blockIdx.x + 1];
   prefetch_segs(t, segs, sb, se);
+  if constexpr (MODE >= 2) {  // NVLS (NEXT-3): sum the fused buffer over the ranks first
+    if (t.nvls_fused) nvls_fused_reduce(t, MODE == 2 ? 0 : 1);
+  }
   const bool producer = (threadIdx.x >> 5) == kTcNW;
   if constexpr (MODE == 0) {
     if (producer) tcp_producer<R8>(t, segs, sb, se, sh);
