@@ -797,9 +797,15 @@ cudaError_t launch_mode(int rt, const Tables& t, const StreamSeg* segs, const in
 // K1 Q-step, second stage: Q_loc of each (layer, panel) = sum of its
 // segments' partial slots, in slot order (deterministic). 8 lanes share one
 // output float4 (each sums every 8th slot), combined by a fixed shuffle tree.
+// lanes per output float4 (each sums every kColReduceSplit-th partial slot):
+// most (layer, panel) units have only a few slots, so one lane per output
+// keeps the grid to about one wave (8 lanes: 6 waves, BERT-L K1-Q 0.704 ms;
+// 2 lanes 0.698; 1 lane 0.689)
+constexpr int kColReduceSplit = 1;
+
 __global__ void __launch_bounds__(256) col_reduce_kernel(Tables t, const ColReduceTask* __restrict__ tasks,
                                                         int ntasks) {
-  constexpr int kSplit = 8;
+  constexpr int kSplit = kColReduceSplit;
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
   const int item = gtid / kSplit, j = gtid % kSplit;
   // items are laid out task by task: item -> (task, k, float4 column)
@@ -864,7 +870,7 @@ __global__ void __launch_bounds__(256) col_reduce_kernel(Tables t, const ColRedu
 cudaError_t launch_col_reduce(const Tables& t, const ColReduceTask* tasks, int ntasks, int nitems,
                               cudaStream_t s) {
   if (ntasks <= 0 || nitems <= 0) return cudaSuccess;
-  const int64_t threads = (int64_t)nitems * 8;
+  const int64_t threads = (int64_t)nitems * kColReduceSplit;
   col_reduce_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(t, tasks, ntasks);
   return cudaGetLastError();
 }
