@@ -798,8 +798,8 @@ __device__ void tcd_consumer(const Tables& t, const TcSeg* segs, int sb, int se,
         mbar_wait(&sh.full[stage], phase);
         const float* fB0 = sh.ring + (size_t)stage * sh.stage_floats;
         const bool full = rows_full && (c00 + kDNB * kPBC <= m) && v4;
-#pragma unroll
-        for (int bx = 0; bx < kDNB; ++bx) {
+#pragma unroll 1
+        for (int bx = 0; bx < kDNB; ++bx) {  // not unrolled: 2 CTAs / SM cap registers at 96
         const int64_t c0 = c00 + kPBC * bx;
         const float* fBh = fB0 + bx * R8 * kPBC;
         const float* fBl = fB0 + (kDNB + bx) * R8 * kPBC;
