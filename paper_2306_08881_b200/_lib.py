@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libacp.so")
+# ACP_LIB: load another in-tree build instead (A/B runs of two builds)
+LIB_PATH = os.environ.get("ACP_LIB") or os.path.join(HERE, "lib", "libacp.so")
 
 ACP_OK, ACP_E_INVAL, ACP_E_CUDA, ACP_E_NCCL, ACP_E_NOMEM, ACP_E_STATE = range(6)
 ACP_NO_EF, ACP_NO_REUSE, ACP_SUM, ACP_POWERSGD = 1, 2, 4, 8
