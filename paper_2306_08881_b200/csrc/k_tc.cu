@@ -450,12 +450,16 @@ __device__ void tcq_producer(const Tables& t, const TcSeg* segs, int sb, int se,
         }
       }
       // row factors [row][R8] (P_loc hi, lo, P_orth hi, lo): 16-byte chunks
-      for (int it = lane; it < 4 * tr * (R8 / 4); it += 32) {
-        const int a = it / (tr * (R8 / 4)), rem = it - a * (tr * (R8 / 4));
-        const int i = rem / (R8 / 4), j = rem - i * (R8 / 4);
-        const bool ok = i < nr;
-        cp_async16(dF + (a * tr + i) * RS + 4 * j, fr[a] + (ok ? (r0 + i) * R8 + 4 * j : 0),
-                   ok ? 16u : 0u);
+      // (R8 / 4 per row: shifts and masks only, no runtime division)
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const float* src = fr[a] + r0 * R8;
+        float* dst = dF + a * tr * RS;
+        for (int it = lane; it < tr * (R8 / 4); it += 32) {
+          const int i = it / (R8 / 4), j = it % (R8 / 4);
+          const bool ok = i < nr;
+          cp_async16(dst + i * RS + 4 * j, ok ? src + i * R8 + 4 * j : src, ok ? 16u : 0u);
+        }
       }
       cp_async_arrive(&sh.full[stage]);
       if (++stage == sh.stages) {

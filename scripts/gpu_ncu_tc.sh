@@ -4,4 +4,4 @@ W=${1:-bert-large-r8}
 T=${2:-tc}
 SMALL="bench.py --workload $W --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-powersgd --secondary none"
 timeout 300 python $SMALL > gpurun_out/bench_small.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"tc_kernel" -s 4 -c 4 -o gpurun_out/prof_$T python $SMALL > gpurun_out/ncu_full.log 2>&1; echo ncu_rc=$?
+timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"${KREGEX:-tc_kernel}" -s ${SKIP:-4} -c ${COUNT:-4} -o gpurun_out/prof_$T python $SMALL > gpurun_out/ncu_full.log 2>&1; echo ncu_rc=$?
