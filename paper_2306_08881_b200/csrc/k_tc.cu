@@ -92,6 +92,9 @@ __device__ __forceinline__ void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 __device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+__device__ __forceinline__ void group_bar(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
 
 // Stage release with S written back by TMA: thread 0 of the consumers
 // releases a stage only after the store that reads it has read it; the
@@ -538,6 +541,17 @@ __device__ void tcq_consumer(const Tables& t, const TcSeg* segs, int sb, int se,
       offa1[j] = box + swz(2 * tq + 1, w >> 2) + (w & 3);
       offb1[j] = box + swz(2 * tq + 1, (w + 8) >> 2) + (w & 3);
     }
+    // the S tile goes back per 32-column box: its writers (the wr row-group
+    // warps of the one or two column groups covering it) meet at named
+    // barrier 2 + box and the first of them stores it, so no warp waits on
+    // the whole CTA each tile. A CTA-wide barrier first: the ids / counts of
+    // this segment must not meet a slower warp of the previous one.
+    const int cpb = 2 / CBW;                      // column groups per box
+    const int mybox = (cg * CBW * 16) >> 5;
+    const bool boxed = tst && mybox < nbox;
+    const bool storer = boxed && rg == 0 && (cg % cpb) == 0;
+    const int bwriters = 32 * mp.wr * cpb;
+    consumers_sync();
     for (int64_t r0 = s.row0; r0 < s.row1; r0 += tr) {
       mbar_wait(&sh.full[stage], phase);
       const float* sM = sh.ring + (size_t)stage * sh.stage_floats;
@@ -636,11 +650,14 @@ __device__ void tcq_consumer(const Tables& t, const TcSeg* segs, int sb, int se,
           acc[j][kb][2] += ta[j][kb][2];
           acc[j][kb][3] += ta[j][kb][3];
         }
-      if (tst) fence_async_smem();
-      consumers_sync();
-      if (threadIdx.x == 0) {
-        if (tst) {
-          for (int b = 0; b < nbox; ++b) tma_store_2d(smap, sS + b * tr * 32, (int)(c0 + 32 * b), (int)r0);
+      if (boxed) {
+        fence_async_smem();
+        group_bar(2 + mybox, bwriters);
+      }
+      __syncwarp();
+      if (lane == 0) {
+        if (storer) {
+          tma_store_2d(smap, sS + mybox * tr * 32, (int)(c0 + 32 * mybox), (int)r0);
           rel.after_store(sh, stage);
         } else {
           rel.immediate(sh, stage);
@@ -669,7 +686,7 @@ __device__ void tcq_consumer(const Tables& t, const TcSeg* segs, int sb, int se,
       }
     }
   }
-  if (threadIdx.x == 0) rel.finish();
+  if (lane == 0) rel.finish();
 }
 
 // ---- decode (K3 on the tensor cores): grad = scale * A B^T, tile = 128 rows
@@ -869,8 +886,8 @@ tc_kernel(Tables t, const TcSeg* __restrict__ segs, const int32_t* __restrict__ 
   if (threadIdx.x == 0) {
     for (int i = 0; i < stages; ++i) {
       mbar_init(&sh.full[i], 33);      // lane 0's expect-tx arrive + one noinc arrive per lane
-      // Q-step K1: consumer thread 0 releases (after the S store read it); else one per warp
-      mbar_init(&sh.empty[i], MODE == 1 ? 1 : kTcNW);
+      // one arrival per consumer warp (Q-step K1: a box's storer after its store read it)
+      mbar_init(&sh.empty[i], kTcNW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
