@@ -583,7 +583,7 @@ __device__ void tcq_consumer(const Tables& t, const TcSeg* segs, int sb, int se,
         }
       }
       auto kstep = [&](const int kk, const int ks) {  // kk: k-step index relative to ks0 (unrolled)
-        const int fo = 8 * RS * kk;  // kk = 1 only happens with wr = 1 (tr = 16)
+        const int fo = 8 * RS * kk;  // kk: rows 8 kk below the warp's first k-step
         const int xo = 256 * kk;
         // B fragments: P_loc (k = rank, n = row) and P_orth (k = row, n = rank)
         uint32_t lbh[KB][2], lbl[KB][2], pbh[KB][2], pbl[KB][2];
@@ -639,8 +639,14 @@ __device__ void tcq_consumer(const Tables& t, const TcSeg* segs, int sb, int se,
             mma3(ta[j][nb], xh, xl, pbh[nb][0], pbh[nb][1], pbl[nb][0], pbl[nb][1]);
         }
       };
-      if (ks0 < ksteps) kstep(0, ks0);
-      if (ks0 + mp.wr < ksteps) kstep(1, ks0 + mp.wr);
+      if constexpr (R8 >= 32) {  // 32-row tiles (tc_q_map): up to 4 k-steps per warp
+        if (ks0 < ksteps) kstep(0, ks0);
+#pragma unroll 1
+        for (int ks = ks0 + mp.wr; ks < ksteps; ks += mp.wr) kstep(ks - ks0, ks);
+      } else {  // 16-row tiles: a second k-step only with wr = 1
+        if (ks0 < ksteps) kstep(0, ks0);
+        if (ks0 + mp.wr < ksteps) kstep(1, ks0 + mp.wr);
+      }
 #pragma unroll
       for (int j = 0; j < CBW; ++j)
 #pragma unroll
@@ -945,7 +951,10 @@ int tc_q_map(int64_t m, int r8, TcMap* out) {
   int wc = 1;
   while (wc < need && wc < kTcNW) wc <<= 1;
   const int wr = kTcNW / wc;
-  const int tr = 8 * (wr > 2 ? wr : 2);
+  // >= 2 k-steps per tile; 4 at r = 32 (narrow panels: longer tiles amortise
+  // the per-tile handshakes; r = 8 / 16 prefer the deeper ring of 16-row tiles)
+  const int ksmin = r8 >= 32 ? 4 : 2;
+  const int tr = 8 * (wr > ksmin ? wr : ksmin);
   out->pc = (int32_t)pc;
   out->np = (int16_t)np;
   out->wc = (int16_t)wc;
