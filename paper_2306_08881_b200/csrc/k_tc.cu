@@ -830,6 +830,55 @@ __device__ void tcd_consumer(const Tables& t, const TcSeg* segs, int sb, int se,
         const int64_t c0 = c00 + kPBC * bx;
         const float* fBh = fB0 + bx * R8 * kPBC;
         const float* fBl = fB0 + (kDNB + bx) * R8 * kPBC;
+        if constexpr (R8 <= 16) {
+        // JB 8-column blocks per batch: all their shared loads first, then the
+        // MMAs, then the global stores (loads of a later batch cannot move
+        // above stores the compiler cannot prove disjoint; batching gives the
+        // MMA chains independent neighbours)
+        constexpr int JB = R8 <= 8 ? 4 : 2;  // r = 32: streamed pairs (registers)
+#pragma unroll
+        for (int j0 = 0; j0 < kPBC / 8; j0 += JB) {
+        uint32_t bfr[JB][KB][4];
+#pragma unroll
+        for (int u = 0; u < JB; ++u) {
+#pragma unroll
+          for (int kb = 0; kb < KB; ++kb) {
+            const int o0 = offL0[j0 + u] + 256 * kb, o1 = offL1[j0 + u] + 256 * kb;
+            if constexpr (MODE == 2) {
+              bfr[u][kb][0] = lds_u32(fBh + o0);
+              bfr[u][kb][1] = lds_u32(fBh + o1);
+              bfr[u][kb][2] = lds_u32(fBl + o0);
+              bfr[u][kb][3] = lds_u32(fBl + o1);
+            } else {
+              split_tf32(fBh[o0], bfr[u][kb][0], bfr[u][kb][2]);
+              split_tf32(fBh[o1], bfr[u][kb][1], bfr[u][kb][3]);
+            }
+          }
+        }
+        float cc[JB][4];
+#pragma unroll
+        for (int u = 0; u < JB; ++u) {
+          cc[u][0] = cc[u][1] = cc[u][2] = cc[u][3] = 0.f;
+#pragma unroll
+          for (int kb = 0; kb < KB; ++kb)
+            mma3(cc[u], ah[kb], al[kb], bfr[u][kb][0], bfr[u][kb][1], bfr[u][kb][2], bfr[u][kb][3]);
+          if constexpr (MODE == 3) {
+#pragma unroll
+            for (int h = 0; h < 4; ++h) cc[u][h] *= scale;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < JB; u += 2) {
+          const int jp = j0 + u;
+          if (full) {
+            store_pair(Ga, Gb, c0 + colj[jp], c0 + colj[jp + 1], tq & 1, cc[u], cc[u + 1]);
+          } else {
+            store_own(Ga, Gb, c0 + colj[jp], m, oka, okb, cc[u]);
+            store_own(Ga, Gb, c0 + colj[jp + 1], m, oka, okb, cc[u + 1]);
+          }
+        }
+        }
+        } else {
 #pragma unroll
         for (int jp = 0; jp < kPBC / 8; jp += 2) {
         float cc[2][4];
@@ -863,6 +912,7 @@ __device__ void tcd_consumer(const Tables& t, const TcSeg* segs, int sb, int se,
         } else {
           store_own(Ga, Gb, c0 + colj[jp], m, oka, okb, cc[0]);
           store_own(Ga, Gb, c0 + colj[jp + 1], m, oka, okb, cc[1]);
+        }
         }
         }
         }
