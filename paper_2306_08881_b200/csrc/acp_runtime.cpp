@@ -100,11 +100,23 @@ struct Plan {
 };
 
 // Split `units` into `grid` contiguous, cost-balanced CTA ranges of segments.
+// Fixed cost of one segment (factor loads into registers / shared memory,
+// the ring's first tile), in byte equivalents, per launch kind: without it
+// CTAs that get many small layers (ResNet) finish last. Measured on 1x B200
+// (profiles/r01_v8_balance.md): 96 KB for the SIMT kernels, 160 KB for the
+// tensor-core K1, 0 for the tensor-core decodes. ACP_SEG_COST_KB overrides.
+enum SegKind { kSegStream = 0, kSegRow = 1, kSegCol = 2, kSegTcK1 = 3, kSegTcDec = 4 };
+double seg_cost_bytes(SegKind k) {
+  if (const char* e = std::getenv("ACP_SEG_COST_KB")) return std::atof(e) * 1024.0;
+  static const double kb[5] = {96, 96, 96, 160, 0};
+  return kb[k] * 1024.0;
+}
+
 template <class Emit>
 int split_units(const std::vector<Unit>& units, int nsm, double min_share, int max_grid,
-                std::vector<int32_t>& ctab, Emit emit) {
+                std::vector<int32_t>& ctab, double seg_cost, Emit emit) {
   double total = 0;
-  for (const Unit& u : units) total += u.cost * (double)u.count;
+  for (const Unit& u : units) total += u.cost * (double)u.count + seg_cost;
   if (total <= 0) {
     ctab.push_back(0);
     return 0;
@@ -114,7 +126,7 @@ int split_units(const std::vector<Unit>& units, int nsm, double min_share, int m
   // whole waves: a multiple of the SM count (max_grid is one), so every SM
   // gets the same number of equal shares
   if (grid > nsm && nsm > 0) grid = std::min(max_grid, (grid + nsm - 1) / nsm * nsm);
-  const double share = total / grid;
+  const double share = (total + seg_cost * grid) / grid;  // + one split segment per CTA
   const size_t cb0 = ctab.size();
   int nseg = 0;
   ctab.push_back(0);
@@ -123,8 +135,8 @@ int split_units(const std::vector<Unit>& units, int nsm, double min_share, int m
   for (const Unit& u : units) {
     int64_t pos = 0;
     while (pos < u.count) {
-      const double budget = share * (cta + 1) - done;
-      int64_t take = (int64_t)std::ceil(budget / u.cost);
+      const double budget = share * (cta + 1) - done - seg_cost;
+      int64_t take = (int64_t)std::ceil(std::max(0.0, budget) / u.cost);
       take = (take + u.align - 1) / u.align * u.align;
       // segment boundaries stay on multiples of align (TC tiles must not
       // straddle two segments): never less than one aligned chunk
@@ -132,7 +144,7 @@ int split_units(const std::vector<Unit>& units, int nsm, double min_share, int m
       take = std::min(take, u.count - pos);
       emit(u, pos, pos + take);
       ++nseg;
-      done += u.cost * (double)take;
+      done += u.cost * (double)take + seg_cost;
       pos += take;
       if (done >= share * (cta + 1) - 1e-6 * share && cta < grid - 1) {
         ++cta;
@@ -324,7 +336,7 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
     const int grid_cap = (one_wave && (mode == 1 || mode == 2 || mode == 3))
                              ? std::min(max_grid, nsm * std::max(1, row_kernel_ctas_per_sm(mode, P.RT)))
                              : max_grid;
-    ln.ncta = split_units(units, nsm, min_share, grid_cap, P.ctab, [&](const Unit& u, int64_t a, int64_t b) {
+    ln.ncta = split_units(units, nsm, min_share, grid_cap, P.ctab, seg_cost_bytes(kSegRow), [&](const Unit& u, int64_t a, int64_t b) {
       RowSeg s{};
       s.layer = u.layer;
       s.row0 = a;
@@ -365,7 +377,7 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
       const int cnt = (int)(P.colsegs.size() - panel_first);
       for (size_t k = panel_first; k < P.colsegs.size(); ++k) P.colsegs[k].pcount = cnt;
     };
-    ln.ncta = split_units(units, nsm, min_share, max_grid, P.ctab, [&](const Unit& u, int64_t a, int64_t b) {
+    ln.ncta = split_units(units, nsm, min_share, max_grid, P.ctab, seg_cost_bytes(kSegCol), [&](const Unit& u, int64_t a, int64_t b) {
       ColSeg s{};
       s.layer = u.layer;
       s.panel = u.panel;
@@ -429,7 +441,9 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
       for (int pn = 0; pn < np; ++pn) {
         const int64_t cols = std::min<int64_t>(pc, L.m - (int64_t)pn * pc);
         // time-weighted cost (generic path ~8x, sub-warp rows ~2x per byte)
-        const double mult = fast ? (mp.lg < 32 ? 2.0 : 1.0) : 8.0;
+        static const double w_sub = std::getenv("ACP_W_SUBWARP") ? std::atof(std::getenv("ACP_W_SUBWARP")) : 2.0;
+        static const double w_gen = std::getenv("ACP_W_GENERIC") ? std::atof(std::getenv("ACP_W_GENERIC")) : 8.0;
+        const double mult = fast ? (mp.lg < 32 ? w_sub : 1.0) : w_gen;
         units.push_back({i, pn, L.n, bpe * (double)cols * mult, tr});
       }
       bytes += bpe * (double)L.n * (double)L.m;
@@ -461,7 +475,7 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
     int64_t part = 0;
     int prev_layer = -1, prev_panel = -1;
     ln.red_off = (int64_t)P.redtasks.size();
-    ln.ncta = split_units(units, nsm, min_share, nsm * cps * stream_waves, P.ctab, [&](const Unit& u, int64_t a, int64_t b) {
+    ln.ncta = split_units(units, nsm, min_share, nsm * cps * stream_waves, P.ctab, seg_cost_bytes(kSegStream), [&](const Unit& u, int64_t a, int64_t b) {
       StreamSeg s{};
       s.layer = u.layer;
       s.row0 = a;
@@ -552,7 +566,8 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
     int64_t part = 0;
     int prev_layer = -1, prev_panel = -1;
     ln.red_off = (int64_t)P.redtasks.size();
-    ln.ncta = split_units(units, nsm, min_share, nsm * tc_cps, P.ctab, [&](const Unit& u, int64_t a, int64_t b) {
+    ln.ncta = split_units(units, nsm, min_share, nsm * tc_cps, P.ctab,
+                          seg_cost_bytes(mode >= 2 ? kSegTcDec : kSegTcK1), [&](const Unit& u, int64_t a, int64_t b) {
       TcSeg sg{};
       sg.layer = u.layer;
       sg.row0 = a;
