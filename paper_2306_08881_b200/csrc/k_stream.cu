@@ -360,7 +360,6 @@ __device__ void seg_fast(const Tables& t, const LayerDesc& L, const StreamSeg& s
   }
   float* __restrict__ E = t.E + L.e_off + c0;      // panel origin (global)
   grad += c0;
-  const float* __restrict__ Pf = t.pbuf + L.p_off;  // k-major [r][n]
 
   // factor(s) in registers for the whole segment (k >= r and invalid chunks: 0)
   float4 qa[MODE == 3 ? 1 : NC][MODE == 3 ? 1 : RT];

@@ -493,7 +493,6 @@ __device__ void tcq_consumer(const Tables& t, const TcSeg* segs, int sb, int se,
     }
     const TcSeg s = segs[si];
     const LayerDesc& L = t.layers[s.layer];
-    float* grad = t.grads[s.layer];
     const int64_t m = L.m;
     const int r = L.r;
     const TcMap mp = L.tq;
