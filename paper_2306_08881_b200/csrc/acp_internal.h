@@ -10,6 +10,8 @@ namespace acp {
 constexpr int kThreads = 256;          // every hot kernel runs 256-thread CTAs
 constexpr int kMaxV = 8;               // row kernel: float4 chunks per thread per row
 constexpr int kOrthRowsPerSeg = 256;   // K2 work unit (factor rows), staged at once
+constexpr int kOrthRowsPerSegLarge = 1024;  // K2 unit at rank <= 2 (<= 4 forced) when a phase has
+                                           // >= one item per SM (fewer queue rounds)
 
 // Thread mapping of a matrix layer onto a TMA stream kernel CTA (NW warps):
 // a row is covered by `gw` warps (lg = 32) or by `lg` lanes of one warp
@@ -255,7 +257,7 @@ int stream_ctas_per_sm(int mode);
 size_t stream_smem_bytes(int stages, int stage_floats, int factor_floats, int ptile);
 // K2: CholeskyQR2 of the factors named by segs (side 0: Q factors in the
 // Q-buffer, length m; side 1: P factors in the P-buffer, length n).
-cudaError_t launch_orth(int rt, const Tables& t, int side, const OrthSeg* segs, int nseg,
+cudaError_t launch_orth(int rt, int seg_rows, const Tables& t, int side, const OrthSeg* segs, int nseg,
                         uint64_t seed, int64_t step, cudaStream_t stream, int* launches);
 // Fill factor slots with counter-based N(0,1) (tag, step): side as above, or
 // side 2 = Q_0 into the Q-buffer. Layers = all matrices. step < 0: use the

@@ -87,6 +87,7 @@ struct Plan {
   std::vector<Launch> k1_b[2];  // WFBP API: one projection launch per bucket
   std::vector<std::pair<int, int>> groups[2];  // [first bucket, last bucket]
   double orth_bytes[2] = {0, 0};
+  int orth_seg[2] = {kOrthRowsPerSeg, kOrthRowsPerSeg};  // K2 rows per work item, per side
   int64_t colpart_elems = 0, colcnt_n = 1, gram_elems = 1;
   // workspace byte offsets
   size_t off_E = 0, off_P = 0, off_Q = 0, off_QL = 0, off_colpart = 0, off_colcnt = 0,
@@ -672,20 +673,42 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
   P.colcnt_n = std::max<int64_t>(P.colcnt_n, P.T);
   if (smem_overflow) return fail(ACP_E_INVAL, "internal: stream kernel shared memory exceeds 227 KB");
   // K2 segments per side (0: Q factors, length m; 1: P factors, length n)
+  // Item size: 1024 rows at rank <= 2 when every SM still gets >= one item
+  // per phase (fewer queue rounds on the chain: BERT-L r = 1 K2 36.6 -> 28.1
+  // us, r = 2 38.8 -> 33.0), else 256 (r = 4 was neutral on BERT-L and slower
+  // on ResNet-152, 33.4 -> 42.2 us; K2). ACP_ORTH_SEG=256|1024
+  // forces it at rank <= 4.
+  int nsm_plan = 148;
+  {
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess)
+      cudaDeviceGetAttribute(&nsm_plan, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const char* seg_env = std::getenv("ACP_ORTH_SEG");
+  for (int side = 0; side < 2; ++side) {
+    int64_t items_large = 0;
+    for (int i = 0; i < P.T; ++i)
+      if (P.L[i].mat)
+        items_large += ((side == 0 ? P.L[i].m : P.L[i].n) + kOrthRowsPerSegLarge - 1) / kOrthRowsPerSegLarge;
+    bool large = P.RT <= 2 && items_large >= nsm_plan;
+    if (seg_env && P.RT <= 4) large = std::atoi(seg_env) == kOrthRowsPerSegLarge;
+    P.orth_seg[side] = large ? kOrthRowsPerSegLarge : kOrthRowsPerSeg;
+  }
   for (int side = 0; side < 2; ++side) {
     int64_t g = 0;
     double bytes = 0;
+    const int64_t segr = P.orth_seg[side];
     for (int i = 0; i < P.T; ++i) {
       const LayerDesc& L = P.L[i];
       if (!L.mat) continue;
       const int64_t len = side == 0 ? L.m : L.n;
-      const int nseg = (int)((len + kOrthRowsPerSeg - 1) / kOrthRowsPerSeg);
+      const int nseg = (int)((len + segr - 1) / segr);
       for (int j = 0; j < nseg; ++j) {
         OrthSeg s{};
         s.layer = i;
         s.seg = j;
-        s.row0 = (int64_t)j * kOrthRowsPerSeg;
-        s.row1 = std::min<int64_t>(len, s.row0 + kOrthRowsPerSeg);
+        s.row0 = (int64_t)j * segr;
+        s.row1 = std::min<int64_t>(len, s.row0 + segr);
         s.gram_off = g;
         s.nseg = nseg;
         g += (int64_t)L.r * L.r;
@@ -912,7 +935,7 @@ acp_status run_orth(acp_ctx* c, int parity, cudaStream_t s) {
   }
   const auto& segs = c->P.orthsegs[side];
   ProfRec* r = prof_begin(c, ACP_K_ORTH, c->P.orth_bytes[side], s);
-  cudaError_t e = launch_orth(c->P.RT, c->tab, side,
+  cudaError_t e = launch_orth(c->P.RT, c->P.orth_seg[side], c->tab, side,
                               reinterpret_cast<const OrthSeg*>(c->ws + c->P.off_orth[side]),
                               (int)segs.size(), c->cfg.seed, -1, s, &nl);
   prof_end(r, s);

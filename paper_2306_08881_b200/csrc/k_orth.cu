@@ -20,12 +20,11 @@
 namespace acp {
 namespace {
 
-constexpr int kSeg = kOrthRowsPerSeg;   // rows staged per CTA (one shot)
-constexpr int kLd = kSeg + 1;           // padded smem row (bank spread)
 constexpr double kDegTol2 = 1e-12;      // (1e-6)^2, reading C6
 
-template <int RT>
+template <int RT, int SEG>
 constexpr size_t orth_smem() {
+  constexpr int kLd = SEG + 1;
   return (size_t)2 * RT * kLd * 4 + (size_t)3 * RT * RT * 8 + kThreads * 8 + 16;
 }
 
@@ -36,9 +35,11 @@ __device__ __forceinline__ long long orth_epoch(int64_t step, int phase) { retur
 // One (phase, segment) work item of K2. Returns after the item; the layer's
 // last segment of phases 0 / 1 also computes W1 / W2 and publishes the
 // layer's next phase through lflag.
-template <int RT>
+template <int RT, int SEG>
 __device__ void orth_item(const Tables& t, int side, const OrthSeg& s, int phase, uint64_t seed,
                           int64_t step, unsigned char* orth_smem_raw) {
+  constexpr int kSeg = SEG;       // rows staged per CTA (one shot)
+  constexpr int kLd = kSeg + 1;   // padded smem row (bank spread)
   float* A = reinterpret_cast<float*>(orth_smem_raw);  // [RT][kLd] input rows (fp32)
   float* B = A + RT * kLd;                               // [RT][kLd] phase-1 output rows
   double* Wm = reinterpret_cast<double*>(B + RT * kLd);  // [RT*RT]
@@ -65,16 +66,19 @@ __device__ void orth_item(const Tables& t, int side, const OrthSeg& s, int phase
     __syncthreads();
   }
 
-  // stage the segment's rows (coalesced along rows, k-major source)
+  // stage the segment's rows (coalesced along rows, k-major source). F, W and
+  // degmask are rewritten inside this launch by other SMs (phase 1 writes F in
+  // place), so every load of them bypasses L1 (__ldcg): a line this SM cached
+  // in an earlier phase would otherwise be read back stale.
   for (int idx = tid; idx < r * kSeg; idx += kThreads) {
     const int k = idx / kSeg, i = idx - k * kSeg;
-    A[k * kLd + i] = i < nr ? F[(int64_t)k * len + s.row0 + i] : 0.f;
+    A[k * kLd + i] = i < nr ? __ldcg(F + (int64_t)k * len + s.row0 + i) : 0.f;
   }
   uint32_t deg = 0;
   if (phase > 0) {
     const double* Wsrc = phase == 1 ? W1 : W2;
-    for (int i = tid; i < r * r; i += kThreads) Wm[i] = Wsrc[i];
-    if (phase == 1) deg = t.degmask[L.deg_idx];
+    for (int i = tid; i < r * r; i += kThreads) Wm[i] = __ldcg(Wsrc + i);
+    if (phase == 1) deg = __ldcg(t.degmask + L.deg_idx);
   }
   __syncthreads();
   const float* G = A;  // rows the Gram is taken of
@@ -237,7 +241,7 @@ __device__ void orth_item(const Tables& t, int side, const OrthSeg& s, int phase
 // items dequeued before it (no deadlock) and a layer's phases follow each
 // other without a grid-wide barrier or a kernel boundary. The last CTA to
 // exit re-arms the queue and advances the step counter (every CTA read it).
-template <int RT>
+template <int RT, int SEG>
 __global__ void __launch_bounds__(kThreads) orth_kernel(Tables t, int side,
                                                         const OrthSeg* __restrict__ segs, int nseg,
                                                         uint64_t seed) {
@@ -253,7 +257,7 @@ __global__ void __launch_bounds__(kThreads) orth_kernel(Tables t, int side,
     __syncthreads();
     if (it >= total) break;
     const int phase = it / nseg;
-    orth_item<RT>(t, side, segs[it - phase * nseg], phase, seed, step, orth_smem_raw);
+    orth_item<RT, SEG>(t, side, segs[it - phase * nseg], phase, seed, step, orth_smem_raw);
   }
   if (threadIdx.x == 0) {
     __threadfence();
@@ -313,9 +317,11 @@ __global__ void transpose_kernel(const float* __restrict__ src, float* __restric
 
 }  // namespace
 
-cudaError_t launch_orth(int rt, const Tables& t, int side, const OrthSeg* segs, int nseg,
+cudaError_t launch_orth(int rt, int seg_rows, const Tables& t, int side, const OrthSeg* segs, int nseg,
                         uint64_t seed, int64_t step, cudaStream_t s, int* launches) {
   if (nseg <= 0) return cudaSuccess;
+  if (seg_rows != kOrthRowsPerSeg && (seg_rows != kOrthRowsPerSegLarge || rt > 4))
+    return cudaErrorInvalidValue;
   (void)step;
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
@@ -332,12 +338,24 @@ cudaError_t launch_orth(int rt, const Tables& t, int side, const OrthSeg* segs, 
   };
   cudaError_t e;
   switch (rt) {
-    case 1: e = go(orth_kernel<1>, orth_smem<1>()); break;
-    case 2: e = go(orth_kernel<2>, orth_smem<2>()); break;
-    case 4: e = go(orth_kernel<4>, orth_smem<4>()); break;
-    case 8: e = go(orth_kernel<8>, orth_smem<8>()); break;
-    case 16: e = go(orth_kernel<16>, orth_smem<16>()); break;
-    case 32: e = go(orth_kernel<32>, orth_smem<32>()); break;
+    case 1:
+      e = seg_rows == kOrthRowsPerSegLarge
+              ? go(orth_kernel<1, kOrthRowsPerSegLarge>, orth_smem<1, kOrthRowsPerSegLarge>())
+              : go(orth_kernel<1, kOrthRowsPerSeg>, orth_smem<1, kOrthRowsPerSeg>());
+      break;
+    case 2:
+      e = seg_rows == kOrthRowsPerSegLarge
+              ? go(orth_kernel<2, kOrthRowsPerSegLarge>, orth_smem<2, kOrthRowsPerSegLarge>())
+              : go(orth_kernel<2, kOrthRowsPerSeg>, orth_smem<2, kOrthRowsPerSeg>());
+      break;
+    case 4:
+      e = seg_rows == kOrthRowsPerSegLarge
+              ? go(orth_kernel<4, kOrthRowsPerSegLarge>, orth_smem<4, kOrthRowsPerSegLarge>())
+              : go(orth_kernel<4, kOrthRowsPerSeg>, orth_smem<4, kOrthRowsPerSeg>());
+      break;
+    case 8: e = go(orth_kernel<8, kOrthRowsPerSeg>, orth_smem<8, kOrthRowsPerSeg>()); break;
+    case 16: e = go(orth_kernel<16, kOrthRowsPerSeg>, orth_smem<16, kOrthRowsPerSeg>()); break;
+    case 32: e = go(orth_kernel<32, kOrthRowsPerSeg>, orth_smem<32, kOrthRowsPerSeg>()); break;
     default: return cudaErrorInvalidValue;
   }
   if (e != cudaSuccess) return e;
