@@ -23,10 +23,17 @@ pytestmark = [pytest.mark.gpu,
 SEED = 2306089
 
 
-@pytest.mark.parametrize("model,rank", [("bert-large", 4), ("resnet50", 4), ("bert-base", 8),
-                                        ("bert-large", 32)])
-def test_full_size_bench_configuration(model, rank):
+# orth_seg: K2 work-item rows forced through ACP_ORTH_SEG (None = the plan's
+# rule). ("bert-large", 1) takes the 1024-row items by default; the forced
+# 1024 at r=4 is the case that exposed stale L1 reads of the factor K2
+# rewrites in place (profiles/r01_v11_k2_items.md).
+@pytest.mark.parametrize("model,rank,orth_seg", [("bert-large", 4, None), ("resnet50", 4, None),
+                                                 ("bert-base", 8, None), ("bert-large", 32, None),
+                                                 ("bert-large", 1, None), ("bert-large", 4, "1024")])
+def test_full_size_bench_configuration(model, rank, orth_seg, monkeypatch):
     import torch
+    if orth_seg is not None:
+        monkeypatch.setenv("ACP_ORTH_SEG", orth_seg)  # read by acp_create's plan
     from paper_2306_08881_b200 import AcpContext
     shapes = [s for _, s in ready_order(model)]
     q0 = make_q0(shapes, rank, SEED)
