@@ -43,16 +43,30 @@
  *
  * Ownership: the caller owns the gradients, the workspace (device memory of at
  * least acp_workspace_bytes()), the CUDA stream and the NCCL communicator.
- * The library allocates no device memory, keeps no gradient pointers across
- * calls, and enqueues all device work asynchronously on the caller's stream
- * (plus one internal stream used for the all-reduces when world_size > 1).
+ * Every device buffer the library uses lives in the caller's workspace (or,
+ * after acp_attach_symmetric, in the caller's symmetric region); the library
+ * itself only creates CUDA streams, events and graph executables. It keeps
+ * the gradient pointers of the last call (a host copy and a device table in
+ * the workspace) only to skip re-uploading an unchanged table; a captured
+ * step graph reads the table, so the pointers passed to a call must stay
+ * valid until the work that call enqueued has finished. All device work is
+ * enqueued asynchronously on the caller's stream (plus one internal stream
+ * for the all-reduces when world_size > 1 or ACP_BUCKETED).
  *
  * Errors: functions return acp_status. ACP_E_INVAL means the arguments were
  * rejected with no side effects; ACP_E_CUDA / ACP_E_NCCL poison the context
- * and every later call on it returns ACP_E_STATE. acp_last_error() returns a
- * thread-local description of the last non-OK status. Non-finite gradients
- * pass through unchecked (as SPEC S:141 does for collectives). All ranks must
- * issue identical parity sequences.
+ * and every later call on it returns ACP_E_STATE. An asynchronous NCCL error
+ * (ncclCommGetAsyncError, polled at the entry of every acp_step /
+ * acp_step_begin / acp_bucket_ready) also poisons it with ACP_E_NCCL.
+ * acp_last_error() returns a thread-local description of the last non-OK
+ * status. Non-finite values: gradients pass through the projections and the
+ * all-reduce unchecked (as SPEC S:141 does for collectives); the
+ * orthogonaliser, whose input must be finite, does not repair a
+ * non-finite factor (NaN propagates to the outputs) but raises a sticky
+ * device flag that acp_check_finite() reports as ACP_E_NONFINITE; with
+ * ACP_CHECK_FINITE every acp_step also scans its all-reduced fused buffer
+ * and checks the flag synchronously (debug mode). All ranks must issue
+ * identical parity sequences.
  */
 #ifndef ACP_H
 #define ACP_H
@@ -74,7 +88,11 @@ typedef enum {
   ACP_E_CUDA = 2,   /* a CUDA call failed; context poisoned                  */
   ACP_E_NCCL = 3,   /* an NCCL call failed; context poisoned                 */
   ACP_E_NOMEM = 4,  /* workspace smaller than acp_workspace_bytes()          */
-  ACP_E_STATE = 5   /* context poisoned by an earlier failure                */
+  ACP_E_STATE = 5,  /* context poisoned by an earlier failure, or a call that
+                       a plan-only context (acp_plan_create) cannot serve   */
+  ACP_E_NONFINITE = 6 /* a non-finite value reached the orthogonaliser or the
+                       all-reduced buffer (acp_check_finite / ACP_CHECK_FINITE);
+                       context poisoned                                     */
 } acp_status;
 
 /* flags */
@@ -84,7 +102,7 @@ enum {
                          factor each step instead of the previous aggregated
                          one (ablation, C12)                            */
   ACP_SUM = 4u,       /* decoded gradient = sum over workers (default: / p)   */
-  ACP_POWERSGD = 8u   /* run the Power-SGD baseline instead (Alg. 1;
+  ACP_POWERSGD = 8u,  /* run the Power-SGD baseline instead (Alg. 1;
                          NEXT-1): each step projects twice, P = M'Q -> AR(P) ->
                          orth(P) -> Q = M'^T P -> AR(Q), E = M' - P Q_loc^T,
                          decoded = P Q^T / p. acp_step ignores parity; in the
@@ -93,6 +111,16 @@ enum {
                          Q, acp_decompress(1) decodes (acp_decompress(0) is a
                          no-op). Needs error feedback and rank <= 8; not
                          combinable with ACP_NO_EF / ACP_NO_REUSE            */
+  ACP_BUCKETED = 16u, /* run the multi-rank scheduler (compute groups, the comm
+                         stream, one NCCL all-reduce per bucket inside an NCCL
+                         group, events, graph capture) even at world_size == 1;
+                         needs nccl_comm (a 1-rank communicator). Lets one GPU
+                         exercise the whole all-reduce path (P:223 / P:228)   */
+  ACP_CHECK_FINITE = 32u /* debug: after each acp_step scan the all-reduced fused
+                         buffer for non-finite values and synchronise the
+                         stream; the step returns ACP_E_NONFINITE on a hit or
+                         when the orthogonaliser saw a non-finite factor
+                                                                    */
 };
 
 typedef struct {
@@ -127,6 +155,21 @@ acp_status acp_workspace_bytes(const acp_config* cfg, size_t* out_bytes);
  * Synchronous (returns after the device work is done). */
 acp_status acp_create(const acp_config* cfg, acp_ctx** out_ctx);
 
+/* Plan-only context: the host part of acp_create (shape policy, r_i, slot
+ * offsets, buckets of both parities, C7-C10) with no device, no
+ * workspace and no communicator -- cfg->device, workspace and nccl_comm are
+ * ignored and the work split assumes 148 SMs. acp_plan_info,
+ * acp_num_buckets, acp_bucket_range and acp_destroy serve it; every other
+ * call returns ACP_E_STATE. Used to check on CPU hosts that all ranks derive
+ * the same bucket sequence. ACP_E_INVAL on a bad shape config. */
+acp_status acp_plan_create(const acp_config* cfg, acp_ctx** out_ctx);
+
+/* Non-finite check: synchronises cuda_stream, then returns
+ * ACP_E_NONFINITE (and poisons the context) if the orthogonaliser saw a
+ * non-finite factor -- or, with ACP_CHECK_FINITE, a step's all-reduced buffer
+ * held a non-finite value -- since the context was created; ACP_OK otherwise. */
+acp_status acp_check_finite(acp_ctx* ctx, void* cuda_stream);
+
 /* One ACP-SGD step (see top). grads: host array of num_tensors DEVICE
  * pointers, each to the tensor's fp32 contiguous gradient, overwritten with
  * the decoded mean. parity: 0 = P-step, 1 = Q-step. cuda_stream: a
@@ -158,7 +201,10 @@ acp_status acp_decompress(acp_ctx* ctx, int32_t parity, float* const* grads, voi
  *   acp_step_end(ctx, s)                    wait for every bucket's all-reduce,
  *                                           decode all tensors into grads
  * Every bucket must be made ready exactly once between begin and end, in any
- * order. Eager launches (no CUDA graph). Errors: ACP_E_INVAL on a bucket
+ * order: the projection runs at once, but the all-reduces are issued strictly
+ * in bucket-index order (a bucket that becomes ready before a lower-indexed
+ * one waits for it), so every rank issues the same collective sequence even
+ * when its hooks fire in a different order. Eager launches (no CUDA graph). Errors: ACP_E_INVAL on a bucket
  * index out of range / a bucket made ready twice / calls out of order
  * (context not poisoned); CUDA / NCCL failures poison the context. */
 acp_status acp_step_begin(acp_ctx* ctx, int32_t parity, float* const* grads, void* cuda_stream);

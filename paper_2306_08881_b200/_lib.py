@@ -12,15 +12,15 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 # ACP_LIB: load another in-tree build instead (A/B runs of two builds)
 LIB_PATH = os.environ.get("ACP_LIB") or os.path.join(HERE, "lib", "libacp.so")
 
-ACP_OK, ACP_E_INVAL, ACP_E_CUDA, ACP_E_NCCL, ACP_E_NOMEM, ACP_E_STATE = range(6)
-ACP_NO_EF, ACP_NO_REUSE, ACP_SUM, ACP_POWERSGD = 1, 2, 4, 8
+ACP_OK, ACP_E_INVAL, ACP_E_CUDA, ACP_E_NCCL, ACP_E_NOMEM, ACP_E_STATE, ACP_E_NONFINITE = range(7)
+ACP_NO_EF, ACP_NO_REUSE, ACP_SUM, ACP_POWERSGD, ACP_BUCKETED, ACP_CHECK_FINITE = 1, 2, 4, 8, 16, 32
 ACP_ABI_VERSION = 1
 (ACP_K_ORTH, ACP_K_PROJ_P, ACP_K_PROJ_Q, ACP_K_DECODE_P, ACP_K_DECODE_Q,
  ACP_K_ALLREDUCE) = range(6)
 KERNEL_CLASS_NAMES = ("orth", "proj_p", "proj_q", "decode_p", "decode_q", "allreduce")
 
 EXPORTED = (
-    "acp_workspace_bytes", "acp_create", "acp_step", "acp_compress", "acp_decompress",
+    "acp_workspace_bytes", "acp_create", "acp_plan_create", "acp_check_finite", "acp_step", "acp_compress", "acp_decompress",
     "acp_get_state", "acp_set_state", "acp_plan_info", "acp_num_buckets", "acp_bucket_range",
     "acp_profile_enable", "acp_profile_reset", "acp_profile_read", "acp_launch_count",
     "acp_set_graphs", "acp_step_begin", "acp_bucket_ready", "acp_step_end",
@@ -71,6 +71,8 @@ def load() -> C.CDLL:
     sig = {
         "acp_workspace_bytes": [C.POINTER(AcpConfig), C.POINTER(sz)],
         "acp_create": [C.POINTER(AcpConfig), C.POINTER(vp)],
+        "acp_plan_create": [C.POINTER(AcpConfig), C.POINTER(vp)],
+        "acp_check_finite": [vp, vp],
         "acp_step": [vp, i32, fpp, vp],
         "acp_compress": [vp, i32, fpp, C.POINTER(vp), C.POINTER(i64), vp],
         "acp_decompress": [vp, i32, fpp, vp],

@@ -69,6 +69,74 @@ def nccl_comm_destroy(comm: int) -> None:
     L.check(L.load().acp_nccl_comm_destroy(C.c_void_p(comm)))
 
 
+def nccl_comm_single(device: Optional[int] = None) -> int:
+    """A 1-rank NCCL communicator on this process's GPU (no process group
+    needed): with ``ACP_BUCKETED`` it drives the per-bucket all-reduce path on
+    one GPU."""
+    import torch
+    lib = L.load()
+    uid = (C.c_uint8 * 128)()
+    L.check(lib.acp_nccl_unique_id(uid))
+    dev = torch.cuda.current_device() if device is None else device
+    comm = C.c_void_p()
+    L.check(lib.acp_nccl_comm_create(uid, 1, 0, dev, C.byref(comm)))
+    return comm.value
+
+
+def _make_config(shapes, rank, world_size, nccl_comm, seed, bucket_bytes, flags, device):
+    """acp_config for parameter shapes in ready order; returns (cfg, keep)
+    where keep holds the ctypes arrays the config points to."""
+    rows, cols = _shape_rows_cols(shapes)
+    T = len(rows)
+    crow = (C.c_int64 * T)(*rows)
+    ccol = (C.c_int64 * T)(*cols)
+    cfg = L.AcpConfig()
+    cfg.abi_version = L.ACP_ABI_VERSION
+    cfg.num_tensors = T
+    cfg.rows = C.cast(crow, C.POINTER(C.c_int64))
+    cfg.cols = C.cast(ccol, C.POINTER(C.c_int64))
+    cfg.rank = int(rank)
+    cfg.world_size = int(world_size)
+    cfg.nccl_comm = C.c_void_p(nccl_comm) if nccl_comm else None
+    cfg.seed = int(seed) & 0xFFFFFFFFFFFFFFFF
+    cfg.default_bucket_bytes = int(bucket_bytes)
+    cfg.flags = int(flags)
+    cfg.device = int(device)
+    return cfg, (crow, ccol)
+
+
+def plan_host(shapes: Sequence[Sequence[int]], rank: int, *, world_size: int = 1,
+              bucket_bytes: int = DEFAULT_BUCKET_BYTES, flags: int = 0) -> dict:
+    """The library's fused-buffer plan, built on the host with no GPU
+    (acp_plan_create): per tensor (r_i, P-slot, Q-slot, E offset, P-bucket,
+    Q-bucket) and every bucket's [offset, count) per parity."""
+    lib = L.load()
+    cfg, keep = _make_config([tuple(int(d) for d in s) for s in shapes], rank, world_size, None, 0,
+                             bucket_bytes, flags, -1)
+    ctx = C.c_void_p()
+    L.check(lib.acp_plan_create(C.byref(cfg), C.byref(ctx)))
+    try:
+        out = (C.c_int64 * 6)()
+        tensors = []
+        for i in range(len(shapes)):
+            L.check(lib.acp_plan_info(ctx, i, out))
+            tensors.append(tuple(int(x) for x in out))
+        buckets = []
+        for parity in (0, 1):
+            nb = C.c_int32()
+            L.check(lib.acp_num_buckets(ctx, parity, C.byref(nb)))
+            rng = []
+            for b in range(nb.value):
+                off, cnt = C.c_int64(), C.c_int64()
+                L.check(lib.acp_bucket_range(ctx, parity, b, C.byref(off), C.byref(cnt)))
+                rng.append((off.value, cnt.value))
+            buckets.append(rng)
+    finally:
+        lib.acp_destroy(ctx)
+    del keep
+    return {"tensors": tensors, "buckets": buckets}
+
+
 class AcpContext:
     """ACP-SGD state of one worker for a list of parameter shapes in READY
     order (the order gradients become ready in back-propagation)."""
@@ -85,22 +153,10 @@ class AcpContext:
         self.world_size = int(world_size)
         dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
         self.device = dev
-        rows, cols = _shape_rows_cols(self.shapes)
-        T = len(rows)
-        self._rows = (C.c_int64 * T)(*rows)
-        self._cols = (C.c_int64 * T)(*cols)
-        cfg = L.AcpConfig()
-        cfg.abi_version = L.ACP_ABI_VERSION
-        cfg.num_tensors = T
-        cfg.rows = C.cast(self._rows, C.POINTER(C.c_int64))
-        cfg.cols = C.cast(self._cols, C.POINTER(C.c_int64))
-        cfg.rank = self.rank
-        cfg.world_size = self.world_size
-        cfg.nccl_comm = C.c_void_p(nccl_comm) if nccl_comm else None
-        cfg.seed = int(seed) & 0xFFFFFFFFFFFFFFFF
-        cfg.default_bucket_bytes = int(bucket_bytes)
-        cfg.flags = int(flags)
-        cfg.device = dev.index if dev.index is not None else torch.cuda.current_device()
+        T = len(self.shapes)
+        cfg, self._keep = _make_config(self.shapes, self.rank, self.world_size, nccl_comm, seed,
+                                       bucket_bytes, flags,
+                                       dev.index if dev.index is not None else torch.cuda.current_device())
         q0buf = None
         if q0 is not None:
             parts = []
@@ -198,9 +254,13 @@ class AcpContext:
         L.check(self._lib.acp_compress(self._ctx, int(parity), self._grad_ptrs(grads),
                                        C.byref(buf), C.byref(cnt),
                                        C.c_void_p(_stream_handle(stream))))
-        base = self.workspace.data_ptr()
-        off = buf.value - base
-        return self.workspace[off:off + 4 * cnt.value].view(torch.float32)
+        # the buffer lives in the workspace, or (after attach_symmetric) in
+        # the symmetric region: view whichever allocation holds it
+        holder = self._symm[0] if getattr(self, "_symm", None) else self.workspace
+        off = buf.value - holder.data_ptr()
+        if off < 0 or off + 4 * cnt.value > holder.numel():
+            raise RuntimeError("acp_compress returned a buffer outside the context's allocations")
+        return holder[off:off + 4 * cnt.value].view(torch.float32)
 
     def decompress(self, grads, parity: int, stream=None) -> None:
         L.check(self._lib.acp_decompress(self._ctx, int(parity), self._grad_ptrs(grads),
@@ -229,6 +289,11 @@ class AcpContext:
         L.check(self._lib.acp_plan_info(self._ctx, i, out))
         return tuple(int(x) for x in out)
 
+    def plan(self) -> dict:
+        """Same structure as ``plan_host`` (for verify_plan_across_ranks)."""
+        return {"tensors": [self.plan_info(i) for i in range(len(self.shapes))],
+                "buckets": [self.buckets(0), self.buckets(1)]}
+
     def buckets(self, parity: int) -> List[Tuple[int, int]]:
         nb = C.c_int32()
         L.check(self._lib.acp_num_buckets(self._ctx, parity, C.byref(nb)))
@@ -254,6 +319,11 @@ class AcpContext:
             out[name] = {"ms": ms.value, "launches": n.value, "bytes": by.value}
         return out
 
+    def check_finite(self, stream=None) -> None:
+        """Synchronise and raise AcpError(ACP_E_NONFINITE) if a non-finite
+        factor reached the orthogonaliser since creation."""
+        L.check(self._lib.acp_check_finite(self._ctx, C.c_void_p(_stream_handle(stream))))
+
     def set_graphs(self, enable: bool = True) -> None:
         L.check(self._lib.acp_set_graphs(self._ctx, 1 if enable else 0))
 
@@ -272,3 +342,16 @@ class AcpContext:
             self.close()
         except Exception:
             pass
+
+
+def verify_plan_across_ranks(plan: dict, group=None) -> bool:
+    """True iff every rank of ``group`` derived the same fused-buffer plan
+    (``plan_host`` / ``AcpContext.plan()``): ranks must issue identical bucket
+    sequences, otherwise their all-reduces pair buckets of different
+    sizes. Collective over any torch.distributed backend."""
+    import hashlib
+    import torch.distributed as dist
+    digest = hashlib.sha256(repr((plan["tensors"], plan["buckets"])).encode()).hexdigest()
+    got = [None] * dist.get_world_size(group)
+    dist.all_gather_object(got, digest, group=group)
+    return all(g == got[0] for g in got)

@@ -173,6 +173,7 @@ struct Tables {
   // ranks in the switch (k_nvls.cuh)
   const NvlsArgs* nv;
   FusedSync* fsync;
+  int32_t* nonfinite;  // sticky flag: bit 0 K2 saw a non-finite factor, bit 1 finite scan hit
   int32_t nvls_fused;  // TC path: per layer [M, S, Q_orth hi, lo, Q_loc hi, lo] (P-step
                              // boxes), [M, S] (Q-step boxes of tq.tr rows), [Q slot]: 9 maps
 };
@@ -265,6 +266,8 @@ cudaError_t launch_orth(int rt, int seg_rows, const Tables& t, int side, const O
 // last phase increments it, so a captured CUDA graph stays valid.
 cudaError_t launch_fill(const Tables& t, const LayerDesc* host_layers, int num_tensors, int side,
                         uint64_t seed, int tag, int64_t step, cudaStream_t stream, int* launches);
+// ACP_CHECK_FINITE: *flag |= 2 if any of buf[0, n) is not finite
+cudaError_t launch_finite_scan(const float* buf, int64_t n, int32_t* flag, cudaStream_t stream);
 // k-major slot <-> row-major rows x r (state access)
 cudaError_t launch_transpose(const float* src, float* dst, int64_t rows, int r, int to_kmajor,
                              cudaStream_t stream);

@@ -62,6 +62,7 @@ struct Plan {
   bool defer = false;   // deferred Q-step residual (stream kernels)
   bool psgd = false;    // ACP_POWERSGD: the Power-SGD baseline (NEXT-1)
   bool tc = false;      // tensor-core K1 + double-deferred residual
+  bool bucketed = false;  // multi-rank scheduler (world_size > 1 or ACP_BUCKETED)
   int R8 = 0;           // TC path: rank padded to a multiple of 8
   int64_t qs_elems = 0, ps_elems = 0;  // TC path: split-factor array sizes (floats)
   std::vector<TcSeg> tcsegs;
@@ -96,7 +97,7 @@ struct Plan {
          off_grads = 0, off_rowsegs = 0, off_colsegs = 0, off_streamsegs = 0, off_orth[2] = {0, 0},
          off_ctab = 0, off_step = 0, off_red = 0, off_defer = 0,
          off_qsplit = 0, off_qlsplit = 0, off_psplit = 0, off_plsplit = 0, off_tcsegs = 0,
-         off_tmaps = 0, off_nvargs = 0, off_fsync = 0,
+         off_tmaps = 0, off_nvargs = 0, off_fsync = 0, off_nvepoch = 0, off_nonfinite = 0,
          total = 0;
 };
 
@@ -157,7 +158,8 @@ int split_units(const std::vector<Unit>& units, int nsm, double min_share, int m
   return grid;
 }
 
-acp_status build_plan(const acp_config* cfg, Plan& P) {
+// plan_only: host-only plan (acp_plan_create): no CUDA calls, 148 SMs assumed.
+acp_status build_plan(const acp_config* cfg, Plan& P, bool plan_only = false) {
   if (!cfg) return fail(ACP_E_INVAL, "config is NULL");
   if (cfg->abi_version != ACP_ABI_VERSION) return fail(ACP_E_INVAL, "abi_version mismatch");
   if (cfg->num_tensors < 1) return fail(ACP_E_INVAL, "num_tensors must be >= 1");
@@ -165,13 +167,16 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
   if (cfg->rank < 1) return fail(ACP_E_INVAL, "rank must be >= 1");
   if (cfg->rank > kMaxRank) return fail(ACP_E_INVAL, "rank > 32 is not supported");
   if (cfg->world_size < 1) return fail(ACP_E_INVAL, "world_size must be >= 1");
-  int ndev = 0;
-  if (cudaGetDeviceCount(&ndev) != cudaSuccess || cfg->device < 0 || cfg->device >= ndev)
-    return fail(ACP_E_INVAL, "invalid CUDA device");
-  int nsm = 0;
-  if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, cfg->device) != cudaSuccess)
-    return fail(ACP_E_CUDA, "cannot query SM count");
+  int nsm = 148;
+  if (!plan_only) {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || cfg->device < 0 || cfg->device >= ndev)
+      return fail(ACP_E_INVAL, "invalid CUDA device");
+    if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, cfg->device) != cudaSuccess)
+      return fail(ACP_E_CUDA, "cannot query SM count");
+  }
   P.nsm = nsm;
+  P.bucketed = cfg->world_size > 1 || (cfg->flags & ACP_BUCKETED) != 0;
   P.T = cfg->num_tensors;
   P.ef = !(cfg->flags & ACP_NO_EF);
   P.psgd = (cfg->flags & ACP_POWERSGD) != 0;
@@ -634,7 +639,7 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
       else if (P.defer || !P.ef) P.k3_fused[p] = row_launch(p == 0 ? 1 : (P.defer ? 3 : 2), all, true);
     }
   }
-  if (cfg->world_size > 1) {
+  if (P.bucketed) {
     // measured on 2xB200 after the load-balance work: 1 group 0.197 / 1.114 ms
     // (ResNet-50 / BERT-L r=4), 2 groups 0.200 / 1.124, 4 groups 0.265 / 1.187
     int ngroups = 1;
@@ -678,12 +683,7 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
   // us, r = 2 38.8 -> 33.0), else 256 (r = 4 was neutral on BERT-L and slower
   // on ResNet-152, 33.4 -> 42.2 us; K2). ACP_ORTH_SEG=256|1024
   // forces it at rank <= 4.
-  int nsm_plan = 148;
-  {
-    int dev = 0;
-    if (cudaGetDevice(&dev) == cudaSuccess)
-      cudaDeviceGetAttribute(&nsm_plan, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int nsm_plan = P.nsm;
   const char* seg_env = std::getenv("ACP_ORTH_SEG");
   for (int side = 0; side < 2; ++side) {
     int64_t items_large = 0;
@@ -754,6 +754,8 @@ acp_status build_plan(const acp_config* cfg, Plan& P) {
   P.off_tmaps = take(P.tc ? sizeof(CUtensorMap) * 9 * (size_t)P.T : 0);
   P.off_nvargs = take(sizeof(NvlsArgs));
   P.off_fsync = take(2 * sizeof(FusedSync));
+  P.off_nvepoch = take(4 * (size_t)kNvlsMaxCtas);
+  P.off_nonfinite = take(4);
   P.off_step = take(8);
   P.off_defer = take(8);
   P.off_red = take(sizeof(ColReduceTask) * P.redtasks.size());
@@ -802,10 +804,12 @@ struct acp_ctx {
   NvlsArgs nv{};
   float* mc_base = nullptr;
   int64_t sym_q_off = 0;           // floats: Q buffer inside the symmetric region
-  uint32_t* nvls_epoch = nullptr;  // device, kNvlsMaxCtas counters
+  uint32_t* nvls_epoch = nullptr;  // device (workspace), kNvlsMaxCtas counters
   bool nvls_fusable = false;       // acp_step: all-reduce inside the decode prologue
   std::vector<CUtensorMap> tmaps;  // TC path: host copy of the per-layer TMA maps
   int64_t launches = 0;
+  bool plan_only = false;  // acp_plan_create: host plan, no device state
+  int next_ar = 0;         // WFBP API: next bucket whose all-reduce may be issued
   bool poisoned = false;
   bool profile = false;
   std::vector<ProfRec> prof;
@@ -986,7 +990,22 @@ acp_status set_grads(acp_ctx* c, float* const* grads, cudaStream_t s) {
 
 acp_status check_ctx(acp_ctx* c) {
   if (!c) return fail(ACP_E_INVAL, "ctx is NULL");
+  if (c->plan_only) return fail(ACP_E_STATE, "plan-only context (acp_plan_create): no device state");
   if (c->poisoned) return fail(ACP_E_STATE, "context poisoned by an earlier failure");
+  return ACP_OK;
+}
+
+// an NCCL failure on another rank (or a transport error) surfaces
+// asynchronously; poll it before enqueueing more collectives on the comm.
+acp_status poll_nccl(acp_ctx* c) {
+  if (!c->comm) return ACP_OK;
+  ncclResult_t ar = ncclSuccess;
+  const ncclResult_t r = ncclCommGetAsyncError(c->comm, &ar);
+  if (r != ncclSuccess) ar = r;
+  if (ar != ncclSuccess && ar != ncclInProgress) {
+    c->poisoned = true;
+    return fail(ACP_E_NCCL, std::string("NCCL asynchronous error: ") + ncclGetErrorString(ar));
+  }
   return ACP_OK;
 }
 
@@ -1061,6 +1080,8 @@ acp_status acp_create(const acp_config* cfg, acp_ctx** out) {
   t.nv = reinterpret_cast<const NvlsArgs*>(c->ws + P.off_nvargs);
   t.fsync = reinterpret_cast<FusedSync*>(c->ws + P.off_fsync);
   t.nvls_fused = 0;
+  t.nonfinite = reinterpret_cast<int32_t*>(c->ws + P.off_nonfinite);
+  c->nvls_epoch = reinterpret_cast<uint32_t*>(c->ws + P.off_nvepoch);
 
   DeviceGuard dg(cfg->device);
   cudaStream_t s = nullptr;
@@ -1106,7 +1127,7 @@ acp_status acp_create(const acp_config* cfg, acp_ctx** out) {
   if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return bail(e, "create sync");
   cudaStreamDestroy(s);
   s = nullptr;
-  if (cfg->world_size > 1) {
+  if (P.bucketed) {
     if ((e = cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking)) != cudaSuccess)
       return bail(e, "comm stream");
     const size_t nb = std::max(P.groups[0].size(), P.groups[1].size());
@@ -1117,6 +1138,27 @@ acp_status acp_create(const acp_config* cfg, acp_ctx** out) {
       cudaEventCreateWithFlags(&c->ev_ar[b], cudaEventDisableTiming);
     }
   }
+  *out = c;
+  g_err.clear();
+  return ACP_OK;
+}
+
+acp_status acp_plan_create(const acp_config* cfg, acp_ctx** out) {
+  if (!out) return fail(ACP_E_INVAL, "out is NULL");
+  *out = nullptr;
+  acp_ctx* c = new acp_ctx();
+  acp_status st = build_plan(cfg, c->P, /*plan_only=*/true);
+  if (st != ACP_OK) {
+    delete c;
+    return st;
+  }
+  c->cfg = *cfg;
+  c->cfg.rows = nullptr;
+  c->cfg.cols = nullptr;
+  c->cfg.q0_host = nullptr;
+  c->cfg.workspace = nullptr;
+  c->cfg.nccl_comm = nullptr;
+  c->plan_only = true;
   *out = c;
   g_err.clear();
   return ACP_OK;
@@ -1231,7 +1273,7 @@ acp_status project_and_reduce(acp_ctx* c, int32_t parity, cudaStream_t s) {
 acp_status enqueue_psgd_step(acp_ctx* c, cudaStream_t s) {
   acp_status st;
   const Plan& P = c->P;
-  if (c->cfg.world_size == 1) {
+  if (!P.bucketed) {
     if ((st = run_k1(c, 0, P.k1_all[0], s)) != ACP_OK) return st;
     if ((st = run_orth(c, 1, s)) != ACP_OK) return st;
     if ((st = run_k1(c, 1, P.k1_all[1], s)) != ACP_OK) return st;
@@ -1256,7 +1298,7 @@ acp_status enqueue_step(acp_ctx* c, int32_t parity, cudaStream_t s) {
   acp_status st;
   if ((st = run_orth(c, parity, s)) != ACP_OK) return st;
   const Plan& P = c->P;
-  if (c->cfg.world_size == 1) {
+  if (!P.bucketed) {
     if ((st = run_k1(c, parity, P.k1_all[parity], s)) != ACP_OK) return st;
     if ((st = run_k3(c, parity, P.k3_all[parity], s)) != ACP_OK) return st;
     return ACP_OK;
@@ -1273,6 +1315,27 @@ acp_status enqueue_step(acp_ctx* c, int32_t parity, cudaStream_t s) {
   for (size_t g = 0; g < P.groups[parity].size(); ++g) {
     CK(c, cudaStreamWaitEvent(s, c->ev_ar[g], 0), "stream wait");
     if ((st = run_k3(c, parity, P.k3_g[parity][g], s)) != ACP_OK) return st;
+  }
+  return ACP_OK;
+}
+
+// Sticky non-finite flag: bit 0 set by K2 (non-finite factor),
+// bit 1 by the fused-buffer scan (scan = true: ACP_CHECK_FINITE after a step).
+acp_status check_finite(acp_ctx* c, int parity, cudaStream_t s, bool scan = true) {
+  if (scan) {
+    const float* buf = parity == 0 ? c->tab.pbuf : c->tab.qbuf;
+    CK(c, launch_finite_scan(buf, c->P.arena[parity], c->tab.nonfinite, s), "finite scan");
+    ++c->launches;
+  }
+  int32_t flag = 0;
+  CK(c, cudaMemcpyAsync(&flag, c->tab.nonfinite, 4, cudaMemcpyDeviceToHost, s), "flag read");
+  CK(c, cudaStreamSynchronize(s), "flag sync");
+  if (flag) {
+    c->poisoned = true;
+    return fail(ACP_E_NONFINITE, std::string("non-finite value ") +
+                                     ((flag & 1) ? "in a factor reaching the orthogonaliser" : "") +
+                                     ((flag & 3) == 3 ? " and " : "") +
+                                     ((flag & 2) ? "in the all-reduced fused buffer" : "") + " (SPEC S:63)");
   }
   return ACP_OK;
 }
@@ -1305,8 +1368,10 @@ acp_status acp_step(acp_ctx* c, int32_t parity, float* const* grads, void* strea
   acp_status st = check_ctx(c);
   if (st != ACP_OK) return st;
   if (parity != 0 && parity != 1) return fail(ACP_E_INVAL, "parity must be 0 or 1");
-  if (c->cfg.world_size > 1 && !c->comm)
-    return fail(ACP_E_INVAL, "world_size > 1 needs an NCCL communicator (or use the split API)");
+  if (c->P.bucketed && !c->comm)
+    return fail(ACP_E_INVAL, "world_size > 1 / ACP_BUCKETED needs an NCCL communicator (or use the split API)");
+  if (c->wf_parity >= 0) return fail(ACP_E_INVAL, "acp_step: a bucket step is open (acp_step_begin)");
+  if ((st = poll_nccl(c)) != ACP_OK) return st;
   DeviceGuard dg(c->cfg.device);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if ((st = set_grads(c, grads, s)) != ACP_OK) return st;
@@ -1321,6 +1386,7 @@ acp_status acp_step(acp_ctx* c, int32_t parity, float* const* grads, void* strea
   }
   after_k1(c, parity);
   ++c->step_count;
+  if (c->cfg.flags & ACP_CHECK_FINITE) return check_finite(c, c->P.psgd ? 1 : parity, s);
   return ACP_OK;
 }
 
@@ -1330,8 +1396,9 @@ acp_status acp_step_begin(acp_ctx* c, int32_t parity, float* const* grads, void*
   if (parity != 0 && parity != 1) return fail(ACP_E_INVAL, "parity must be 0 or 1");
   if (c->P.psgd) return fail(ACP_E_INVAL, "the bucket API runs ACP-SGD only (not ACP_POWERSGD)");
   if (c->wf_parity >= 0) return fail(ACP_E_INVAL, "acp_step_begin: a step is already open");
-  if (c->cfg.world_size > 1 && !c->comm)
-    return fail(ACP_E_INVAL, "world_size > 1 needs an NCCL communicator");
+  if (c->P.bucketed && !c->comm)
+    return fail(ACP_E_INVAL, "world_size > 1 / ACP_BUCKETED needs an NCCL communicator");
+  if ((st = poll_nccl(c)) != ACP_OK) return st;
   DeviceGuard dg(c->cfg.device);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if ((st = set_grads(c, grads, s)) != ACP_OK) return st;
@@ -1345,6 +1412,7 @@ acp_status acp_step_begin(acp_ctx* c, int32_t parity, float* const* grads, void*
     c->wf_ev.push_back(ev);
   }
   c->wf_parity = parity;
+  c->next_ar = 0;
   return ACP_OK;
 }
 
@@ -1356,20 +1424,27 @@ acp_status acp_bucket_ready(acp_ctx* c, int32_t b, void* stream) {
   const Plan& P = c->P;
   if (b < 0 || b >= (int32_t)P.buckets[parity].size()) return fail(ACP_E_INVAL, "bucket index out of range");
   if (c->wf_done[b]) return fail(ACP_E_INVAL, "bucket made ready twice");
+  if ((st = poll_nccl(c)) != ACP_OK) return st;
   DeviceGuard dg(c->cfg.device);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if ((st = run_k1(c, parity, P.k1_b[parity][b], s)) != ACP_OK) return st;
-  if (c->cfg.world_size > 1) {
-    cudaEvent_t k1done = c->wf_ev[2 * b], ardone = c->wf_ev[2 * b + 1];
-    CK(c, cudaEventRecord(k1done, s), "event record");
-    CK(c, cudaStreamWaitEvent(c->comm_stream, k1done, 0), "stream wait");
-    ProfRec* r = prof_begin(c, ACP_K_ALLREDUCE, 4.0 * P.bcnt[parity][b], c->comm_stream);
-    st = allreduce_range(c, parity, P.boff[parity][b], P.bcnt[parity][b]);
-    prof_end(r, c->comm_stream);
-    if (st != ACP_OK) return st;
-    CK(c, cudaEventRecord(ardone, c->comm_stream), "event record");
-  }
   c->wf_done[b] = 1;
+  if (P.bucketed) {
+    CK(c, cudaEventRecord(c->wf_ev[2 * b], s), "event record");
+    // collectives strictly in bucket-index order (identical on every rank,
+    // whatever order the hooks fired in): issue every ready prefix bucket
+    const int nb = (int)P.buckets[parity].size();
+    while (c->next_ar < nb && c->wf_done[c->next_ar]) {
+      const int a = c->next_ar;
+      CK(c, cudaStreamWaitEvent(c->comm_stream, c->wf_ev[2 * a], 0), "stream wait");
+      ProfRec* r = prof_begin(c, ACP_K_ALLREDUCE, 4.0 * P.bcnt[parity][a], c->comm_stream);
+      st = allreduce_range(c, parity, P.boff[parity][a], P.bcnt[parity][a]);
+      prof_end(r, c->comm_stream);
+      if (st != ACP_OK) return st;
+      CK(c, cudaEventRecord(c->wf_ev[2 * a + 1], c->comm_stream), "event record");
+      ++c->next_ar;
+    }
+  }
   return ACP_OK;
 }
 
@@ -1382,7 +1457,7 @@ acp_status acp_step_end(acp_ctx* c, void* stream) {
     if (!c->wf_done[b]) return fail(ACP_E_INVAL, "acp_step_end: bucket " + std::to_string(b) + " not ready");
   DeviceGuard dg(c->cfg.device);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  if (c->cfg.world_size > 1)
+  if (c->P.bucketed)
     for (size_t b = 0; b < c->wf_done.size(); ++b)
       CK(c, cudaStreamWaitEvent(s, c->wf_ev[2 * b + 1], 0), "stream wait");
   if ((st = run_k3(c, parity, c->P.k3_all[parity], s)) != ACP_OK) return st;
@@ -1425,10 +1500,7 @@ acp_status acp_attach_symmetric(acp_ctx* c, void* local, void* multicast, void* 
   CK(c, cudaMemcpy(np, c->tab.pbuf, 4 * (size_t)c->P.arena[0], cudaMemcpyDeviceToDevice), "move P buffer");
   CK(c, cudaMemcpy(nq, c->tab.qbuf, 4 * (size_t)c->P.arena[1], cudaMemcpyDeviceToDevice), "move Q buffer");
   CK(c, cudaMemset(base + fo, 0, kNvlsFlagRows * kNvlsMaxCtas * kNvlsMaxRanks * 4), "zero flags");
-  if (!c->nvls_epoch) {
-    CK(c, cudaMalloc(&c->nvls_epoch, 4 * kNvlsMaxCtas), "epoch alloc");
-    CK(c, cudaMemset(c->nvls_epoch, 0, 4 * kNvlsMaxCtas), "epoch zero");
-  }
+  CK(c, cudaMemset(c->nvls_epoch, 0, 4 * kNvlsMaxCtas), "epoch zero");
   c->tab.pbuf = np;
   c->tab.qbuf = nq;
   c->mc_base = reinterpret_cast<float*>(multicast);
@@ -1458,6 +1530,13 @@ acp_status acp_attach_symmetric(acp_ctx* c, void* local, void* multicast, void* 
     }
   std::fill(c->grads_cache.begin(), c->grads_cache.end(), nullptr);
   return ACP_OK;
+}
+
+acp_status acp_check_finite(acp_ctx* c, void* stream) {
+  acp_status st = check_ctx(c);
+  if (st != ACP_OK) return st;
+  DeviceGuard dg(c->cfg.device);
+  return check_finite(c, 0, reinterpret_cast<cudaStream_t>(stream), /*scan=*/false);
 }
 
 acp_status acp_set_graphs(acp_ctx* c, int32_t enable) {
@@ -1604,6 +1683,10 @@ acp_status acp_launch_count(acp_ctx* c, int64_t* out) {
 
 acp_status acp_destroy(acp_ctx* c) {
   if (!c) return ACP_OK;
+  if (c->plan_only) {
+    delete c;
+    return ACP_OK;
+  }
   DeviceGuard dg(c->cfg.device);
   for (auto& ge : c->gexec)
     if (ge) cudaGraphExecDestroy(ge);
@@ -1615,7 +1698,6 @@ acp_status acp_destroy(acp_ctx* c) {
   for (auto ev : c->ev_k1) cudaEventDestroy(ev);
   for (auto ev : c->ev_ar) cudaEventDestroy(ev);
   for (auto ev : c->wf_ev) cudaEventDestroy(ev);
-  if (c->nvls_epoch) cudaFree(c->nvls_epoch);
   for (auto& r : c->prof) {
     cudaEventDestroy(r.a);
     cudaEventDestroy(r.b);

@@ -1,6 +1,7 @@
 // Device helpers shared by the sm_100a kernels.
 #pragma once
 #include <cstdint>
+#include <utility>
 #include <cuda_runtime.h>
 #include "acp_internal.h"
 
@@ -58,6 +59,35 @@ __device__ __forceinline__ float gaussian_at(uint64_t key, uint64_t i) {
   const double u2 = (double)(b >> 11) * 0x1p-53;
   const double z = sqrt(-2.0 * log(u1)) * cos(2.0 * 3.141592653589793 * u2);
   return (float)z;
+}
+
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// Bounded spin (device-side waits on flags other CTAs publish): a broken
+// epoch / counter traps after 10 s instead of hanging the GPU.
+constexpr uint64_t kSpinLimitNs = 10000000000ull;
+
+// Host: launch `kern` on `s`; cooperative = the CTAs of the grid wait on each
+// other (NVLS barriers), so ask for guaranteed co-residency
+// (cudaLaunchAttributeCooperative: the launch fails instead of deadlocking
+// when the grid cannot be resident at once; valid inside graph capture).
+template <class... KArgs, class... Args>
+inline cudaError_t launch_kernel(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                                 cudaStream_t s, bool cooperative, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = cooperative ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
 // mbarrier / async-copy helpers (k_stream.cu, k_tc.cu)

@@ -81,8 +81,8 @@ cudaError_t launch_nvls_allreduce(const NvlsArgs& a, int64_t off, int64_t cnt, c
   if (cnt <= 0) return cudaSuccess;
   const int64_t per4 = (cnt / 4 + a.world - 1) / a.world;
   int grid = (int)std::min<int64_t>(kNvlsMaxCtas, std::max<int64_t>(1, (per4 + 511) / 512));
-  nvls_allreduce_kernel<<<grid, 512, 0, s>>>(a, off, cnt);
-  return cudaGetLastError();
+  // CTA c of every rank meets CTA c of every other rank: co-resident grid
+  return launch_kernel(nvls_allreduce_kernel, dim3(grid), dim3(512), 0, s, true, a, off, cnt);
 }
 
 }  // namespace acp

@@ -21,16 +21,11 @@ __device__ __forceinline__ uint32_t nv_ld_acquire_gpu(const uint32_t* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ uint64_t nv_globaltimer() {
-  uint64_t t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
 __device__ __forceinline__ void nv_wait_ge(const uint32_t* p, uint32_t target, bool sys) {
-  const uint64_t t0 = nv_globaltimer();
+  const uint64_t t0 = globaltimer_ns();
   while ((int)((sys ? nv_ld_acquire_sys(p) : nv_ld_acquire_gpu(p)) - target) < 0) {
     __nanosleep(64);
-    if (nv_globaltimer() - t0 > 10000000000ull) __trap();  // never hang the GPU
+    if (globaltimer_ns() - t0 > kSpinLimitNs) __trap();  // never hang the GPU
   }
 }
 
@@ -84,6 +79,10 @@ __device__ __forceinline__ void nvls_fused_reduce(const Tables& t, int parity) {
   }
   nv_grid_barrier(a, fs, 2u * e + 2u, row + 1);  // every slice is summed everywhere
   if (blockIdx.x == 0 && threadIdx.x == 0) fs->epoch = e + 1u;  // all CTAs read e at entry
+  // the decode reads the summed buffer through TMA / cp.async.bulk (async
+  // proxy) as well as plain loads: order the generic-proxy multimem writes
+  // before them
+  asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
 }  // namespace acp

@@ -60,7 +60,11 @@ __device__ void orth_item(const Tables& t, int side, const OrthSeg& s, int phase
     if (tid == 0) {
       volatile long long* f = t.orthflag + L.deg_idx;
       const long long want = orth_epoch(step, phase);
-      while (*f < want) __nanosleep(64);
+      const uint64_t t0 = globaltimer_ns();
+      while (*f < want) {
+        __nanosleep(64);
+        if (globaltimer_ns() - t0 > kSpinLimitNs) __trap();  // broken epoch: fail loudly
+      }
       __threadfence();
     }
     __syncthreads();
@@ -184,8 +188,11 @@ __device__ void orth_item(const Tables& t, int side, const OrthSeg& s, int phase
   if (tid < 32) {
     const int lane = tid;
     uint32_t dmask = 0;
+    bool nonfinite = false;
     // left-looking Cholesky G = R^T R (R upper), lane l owns column l;
-    // a degenerate column (residual <= 1e-6 of its norm) is dropped (C6)
+    // a degenerate column (residual <= 1e-6 of its norm) is dropped (C6).
+    // A non-finite column is NOT repaired (non-finite input is an
+    // error): it propagates NaN and raises the sticky flag for the host.
     for (int k = 0; k < r; ++k) {
       const double gkk = Gs[k * r + k];
       double d = gkk;
@@ -193,7 +200,9 @@ __device__ void orth_item(const Tables& t, int side, const OrthSeg& s, int phase
         const double rjk = Rm[j * r + k];
         d = fma(-rjk, rjk, d);
       }
-      const bool dg = !(gkk > 0.0) || !(d > kDegTol2 * gkk);
+      const bool fin = isfinite(gkk);
+      nonfinite |= !fin;
+      const bool dg = fin && (!(gkk > 0.0) || !(d > kDegTol2 * gkk));
       const double rkk = dg ? 1.0 : sqrt(d);
       if (dg) dmask |= 1u << k;
       if (lane < r) {
@@ -226,6 +235,7 @@ __device__ void orth_item(const Tables& t, int side, const OrthSeg& s, int phase
       }
     }
     if (lane == 0) {
+      if (nonfinite) atomicOr(t.nonfinite, 1);
       if (phase == 0) t.degmask[L.deg_idx] = dmask;
       t.orthcnt[L.deg_idx] = 0;  // re-arm
       __threadfence();
@@ -302,6 +312,13 @@ __global__ void materialize_kernel(Tables t, int layer, float* dst) {
     for (int k = 0; k < r; ++k) x = fmaf(-P[k * n + i], Ql[k * m + j], x);
     dst[idx] = x;
   }
+}
+
+__global__ void finite_scan_kernel(const float* __restrict__ buf, int64_t n, int32_t* flag) {
+  bool bad = false;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    bad |= !isfinite(buf[i]);
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 2);
 }
 
 __global__ void transpose_kernel(const float* __restrict__ src, float* __restrict__ dst,
@@ -388,6 +405,14 @@ cudaError_t launch_materialize(const Tables& t, const LayerDesc& L, int layer, f
   int64_t blocks = (total + kThreads - 1) / kThreads;
   if (blocks > 8192) blocks = 8192;
   materialize_kernel<<<(unsigned)blocks, kThreads, 0, s>>>(t, layer, dst);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_finite_scan(const float* buf, int64_t n, int32_t* flag, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  int64_t blocks = (n + kThreads - 1) / kThreads;
+  if (blocks > 1184) blocks = 1184;
+  finite_scan_kernel<<<(unsigned)blocks, kThreads, 0, s>>>(buf, n, flag);
   return cudaGetLastError();
 }
 

@@ -164,10 +164,23 @@ __device__ void k1p_fast(const Tables& t, const LayerDesc& L, const float* __res
   }
 }
 
-// ---- mode 1, fast path ----------------------------------------------------
-template <int RT>
+// Factor loads of the decodes. FUSED (NVLS prologue, k_nvls.cuh): the
+// all-reduced slot was rewritten inside this launch by the multicast store,
+// so it is read through L2 (ld.global.cg), never the non-coherent L1 path.
+template <bool CG>
+__device__ __forceinline__ float ld_fac(const float* p) { return CG ? __ldcg(p) : __ldg(p); }
+template <bool CG>
+__device__ __forceinline__ float4 ld_fac4(const float* p) {
+  return CG ? __ldcg(reinterpret_cast<const float4*>(p)) : ld_f4(p);
+}
+
+// ---- mode 1 (and 3), fast path ----------------------------------------------
+// MODE 1: P-step decode (the P slot is the all-reduced one); MODE 3: Q-step
+// decode of the deferred path (the Q slot is the all-reduced one).
+template <int RT, int MODE, bool FUSED>
 __device__ void k3p_fast(const Tables& t, const LayerDesc& L, float* __restrict__ grad,
                          int64_t row0, int64_t row1, float scale) {
+  constexpr bool kCgP = FUSED && MODE == 1, kCgQ = FUSED && MODE == 3;
   constexpr int R = rows_k3p(RT);
   const int G = L.G, V = L.V;
   const int NG = kThreads / G;
@@ -187,7 +200,7 @@ __device__ void k3p_fast(const Tables& t, const LayerDesc& L, float* __restrict_
       const int64_t row = base + rr;
 #pragma unroll
       for (int k = 0; k < RT; ++k)
-        p[rr][k] = (k < r && row < row1) ? __ldg(Pa + k * n + row) * scale : 0.f;
+        p[rr][k] = (k < r && row < row1) ? ld_fac<kCgP>(Pa + k * n + row) * scale : 0.f;
     }
     for (int v = 0; v < V; ++v) {
       const int c = l + v * G;
@@ -198,7 +211,7 @@ __device__ void k3p_fast(const Tables& t, const LayerDesc& L, float* __restrict_
 #pragma unroll
       for (int k = 0; k < RT; ++k) {
         if (k < r) {
-          const float4 q = ld_f4(Qo + k * m + 4 * c);
+          const float4 q = ld_fac4<kCgQ>(Qo + k * m + 4 * c);
 #pragma unroll
           for (int rr = 0; rr < R; ++rr) f4fma(o[rr], p[rr][k], q);
         }
@@ -213,7 +226,7 @@ __device__ void k3p_fast(const Tables& t, const LayerDesc& L, float* __restrict_
 }
 
 // ---- mode 2, fast path ----------------------------------------------------
-template <int RT>
+template <int RT, bool FUSED>
 __device__ void k3q_fast(const Tables& t, const LayerDesc& L, float* __restrict__ grad,
                          int64_t row0, int64_t row1, float scale, int ef) {
   constexpr int R = rows_k3q(RT);
@@ -256,7 +269,7 @@ __device__ void k3q_fast(const Tables& t, const LayerDesc& L, float* __restrict_
 #pragma unroll
       for (int k = 0; k < RT; ++k) {
         if (k < r) {
-          const float4 qa = ld_f4(Qa + k * m + 4 * c);
+          const float4 qa = ld_fac4<FUSED>(Qa + k * m + 4 * c);
 #pragma unroll
           for (int rr = 0; rr < R; ++rr) f4fma(o[rr], p[rr][k], qa);
           if (ef) {
@@ -300,7 +313,7 @@ __device__ __forceinline__ void block_sum(float (&a)[RT], float* red) {
   __syncthreads();
 }
 
-template <int MODE, int RT>
+template <int MODE, int RT, bool CG>
 __device__ void row_generic(const Tables& t, const LayerDesc& L, float* __restrict__ grad,
                             int64_t row0, int64_t row1, float scale, int ef, float* red) {
   // one warp per row (lanes stride the columns, shuffle row sums): layers with
@@ -347,20 +360,20 @@ __device__ void row_generic(const Tables& t, const LayerDesc& L, float* __restri
     } else {
       float p[RT];
 #pragma unroll
-      for (int k = 0; k < RT; ++k) p[k] = (k < r) ? __ldg(Ps + k * n + row) : 0.f;
+      for (int k = 0; k < RT; ++k) p[k] = (k < r) ? ld_fac<CG>(Ps + k * n + row) : 0.f;
       for (int64_t j = lane; j < m; j += 32) {
         float o = 0.f;
         if (MODE == 1) {
 #pragma unroll
           for (int k = 0; k < RT; ++k)
-            if (k < r) o = fmaf(p[k], __ldg(Qs + k * m + j), o);
+            if (k < r) o = fmaf(p[k], ld_fac<CG>(Qs + k * m + j), o);
         } else {
           float x = ef ? g[j] + e[j] : 0.f;
 #pragma unroll
           for (int k = 0; k < RT; ++k) {
             if (k < r) {
-              o = fmaf(p[k], __ldg(Qs + k * m + j), o);
-              if (ef) x = fmaf(-p[k], __ldg(Ql + k * m + j), x);
+              o = fmaf(p[k], ld_fac<CG>(Qs + k * m + j), o);
+              if (ef) x = fmaf(-p[k], ld_fac<CG>(Ql + k * m + j), x);
             }
           }
           if (ef) e[j] = x;
@@ -394,7 +407,7 @@ __global__ void __launch_bounds__(kThreads) row_kernel(Tables t, const RowSeg* _
                        float* slot = (MODE >= 2 ? t.qbuf + L.q_off : t.pbuf + L.p_off);
                        for (int64_t i = sg.row0 + first; i < sg.row1; i += stride) {
                          if (MODE == 0) slot[i] = grad[i];
-                         else grad[i] = slot[i] * scale;
+                         else grad[i] = (t.nvls_fused ? __ldcg(slot + i) : slot[i]) * scale;
                        }
                      }) - 1;
       continue;
@@ -404,7 +417,10 @@ __global__ void __launch_bounds__(kThreads) row_kernel(Tables t, const RowSeg* _
     float* grad = t.grads[sg.layer];
     const bool fast = L.G > 0 && ((reinterpret_cast<uintptr_t>(grad) & 15u) == 0);
     if (!fast) {
-      row_generic<MODE == 3 ? 1 : MODE, RT>(t, L, grad, sg.row0, sg.row1, scale, ef, red_gen);
+      if (MODE != 0 && t.nvls_fused)
+        row_generic<MODE == 3 ? 1 : MODE, RT, true>(t, L, grad, sg.row0, sg.row1, scale, ef, red_gen);
+      else
+        row_generic<MODE == 3 ? 1 : MODE, RT, false>(t, L, grad, sg.row0, sg.row1, scale, ef, red_gen);
       continue;
     }
     if constexpr (MODE == 0) {
@@ -419,9 +435,11 @@ __global__ void __launch_bounds__(kThreads) row_kernel(Tables t, const RowSeg* _
         default: k1p_fast<RT, 8>(t, L, grad, sg.row0, sg.row1, ef, red, phase); break;
       }
     } else if constexpr (MODE == 1 || MODE == 3) {
-      k3p_fast<RT>(t, L, grad, sg.row0, sg.row1, scale);
+      if (t.nvls_fused) k3p_fast<RT, MODE, true>(t, L, grad, sg.row0, sg.row1, scale);
+      else k3p_fast<RT, MODE, false>(t, L, grad, sg.row0, sg.row1, scale);
     } else {
-      k3q_fast<RT>(t, L, grad, sg.row0, sg.row1, scale, ef);
+      if (t.nvls_fused) k3q_fast<RT, true>(t, L, grad, sg.row0, sg.row1, scale, ef);
+      else k3q_fast<RT, false>(t, L, grad, sg.row0, sg.row1, scale, ef);
     }
   }
 }
@@ -430,16 +448,17 @@ template <int MODE>
 cudaError_t launch_row_mode(int rt, const Tables& t, const RowSeg* segs, const int32_t* cb,
                             int ncta, float scale, int ef, cudaStream_t s) {
   dim3 grid(ncta), block(kThreads);
+  // the NVLS-fused decode barriers its whole grid (k_nvls.cuh): cooperative
+  const bool coop = MODE != 0 && t.nvls_fused;
   switch (rt) {
-    case 1: row_kernel<MODE, 1><<<grid, block, 0, s>>>(t, segs, cb, scale, ef); break;
-    case 2: row_kernel<MODE, 2><<<grid, block, 0, s>>>(t, segs, cb, scale, ef); break;
-    case 4: row_kernel<MODE, 4><<<grid, block, 0, s>>>(t, segs, cb, scale, ef); break;
-    case 8: row_kernel<MODE, 8><<<grid, block, 0, s>>>(t, segs, cb, scale, ef); break;
-    case 16: row_kernel<MODE, 16><<<grid, block, 0, s>>>(t, segs, cb, scale, ef); break;
-    case 32: row_kernel<MODE, 32><<<grid, block, 0, s>>>(t, segs, cb, scale, ef); break;
+    case 1: return launch_kernel(row_kernel<MODE, 1>, grid, block, 0, s, coop, t, segs, cb, scale, ef);
+    case 2: return launch_kernel(row_kernel<MODE, 2>, grid, block, 0, s, coop, t, segs, cb, scale, ef);
+    case 4: return launch_kernel(row_kernel<MODE, 4>, grid, block, 0, s, coop, t, segs, cb, scale, ef);
+    case 8: return launch_kernel(row_kernel<MODE, 8>, grid, block, 0, s, coop, t, segs, cb, scale, ef);
+    case 16: return launch_kernel(row_kernel<MODE, 16>, grid, block, 0, s, coop, t, segs, cb, scale, ef);
+    case 32: return launch_kernel(row_kernel<MODE, 32>, grid, block, 0, s, coop, t, segs, cb, scale, ef);
     default: return cudaErrorInvalidValue;
   }
-  return cudaGetLastError();
 }
 
 }  // namespace

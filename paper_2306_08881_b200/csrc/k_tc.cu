@@ -1055,8 +1055,9 @@ cudaError_t launch_tc(int mode, int r8, const Tables& t, const TcSeg* segs, cons
   auto go = [&](auto kern) -> cudaError_t {
     cudaError_t e = allow_max_smem(reinterpret_cast<const void*>(kern));
     if (e != cudaSuccess) return e;
-    kern<<<ncta, kTcNW * 32 + 32, smem, st>>>(t, segs, cb, stages, stage_floats, scale);
-    return cudaGetLastError();
+    // the NVLS-fused decode barriers its whole grid (k_nvls.cuh): cooperative
+    return launch_kernel(kern, dim3(ncta), dim3(kTcNW * 32 + 32), smem, st, mode >= 2 && t.nvls_fused != 0,
+                         t, segs, cb, stages, stage_floats, scale);
   };
   switch (mode * 100 + r8) {
     case 8: return go(tc_kernel<0, 8>);

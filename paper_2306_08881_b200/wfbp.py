@@ -21,7 +21,7 @@ from __future__ import annotations
 
 from typing import Optional
 
-from .acp import AcpContext, DEFAULT_BUCKET_BYTES
+from .acp import AcpContext, DEFAULT_BUCKET_BYTES, verify_plan_across_ranks
 
 
 class Wfbp:
@@ -36,6 +36,14 @@ class Wfbp:
                 p.grad = torch.zeros_like(p, memory_format=torch.contiguous_format)
         self.ctx = AcpContext([tuple(p.shape) for p in self.params], rank, world_size=world_size,
                               nccl_comm=nccl_comm, seed=seed, bucket_bytes=bucket_bytes, flags=flags)
+        if world_size > 1:
+            # every rank must issue the same bucket sequence; the
+            # library issues its all-reduces in bucket-index order whatever
+            # order the hooks fire in, but the buckets themselves must match
+            import torch.distributed as dist
+            if dist.is_available() and dist.is_initialized() and \
+                    not verify_plan_across_ranks(self.ctx.plan()):
+                raise RuntimeError("ranks derived different fused-buffer plans (different parameter lists?)")
         self.overlap = overlap
         self.bucket_of = [[int(self.ctx.plan_info(i)[4 + par]) for i in range(len(self.params))]
                           for par in (0, 1)]

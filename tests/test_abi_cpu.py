@@ -70,3 +70,49 @@ def test_abi_version_and_invalid_config(lib):
     assert lib.acp_workspace_bytes(C.byref(cfg), C.byref(out)) == ACP_E_INVAL
     assert b"abi" in lib.acp_last_error()
     assert lib.acp_step(None, 0, None, None) == ACP_E_INVAL
+
+
+def test_plan_only_context_matches_oracle_plan(lib):
+    """acp_plan_create builds the plan with no GPU; its offsets and buckets
+    equal the oracle's independent restatement (C7-C10) bit for
+    bit, and every call that needs device state is refused (ACP_E_STATE)."""
+    from paper_2306_08881_b200 import plan_host
+    from paper_2306_08881_b200._lib import AcpConfig, ACP_E_STATE, ACP_ABI_VERSION
+    from oracle import fusion_plan
+    from acp_inputs import ready_order
+    for model, rank, bb in [("resnet50", 4, 25 * 2 ** 20), ("bert-base", 8, 25 * 2 ** 20),
+                            ("resnet152", 4, 0), ("resnet152", 4, -1), ("resnet152", 4, 2 ** 20)]:
+        shapes = [s for _, s in ready_order(model)]
+        got = plan_host(shapes, rank, bucket_bytes=bb)
+        want = fusion_plan(shapes, rank, bb)
+        for i, (r, po, qo, eo, bp, bq) in enumerate(got["tensors"]):
+            L = want["layers"][i]
+            assert (r, po, qo, eo) == (L.r, want["slot_off"][0][i], want["slot_off"][1][i], want["e_off"][i])
+            assert i in want["buckets"][0][bp] and i in want["buckets"][1][bq]
+        for parity in (0, 1):
+            assert len(got["buckets"][parity]) == len(want["buckets"][parity])
+            for (off, cnt), members in zip(got["buckets"][parity], want["buckets"][parity]):
+                first, last = members[0], members[-1]
+                assert off == want["slot_off"][parity][first]
+                end = (want["slot_off"][parity][last + 1] if last + 1 < len(shapes)
+                       else want["arena_elems"][parity])
+                assert off + cnt == end
+    # device calls on a plan-only context
+    rows = (C.c_int64 * 2)(64, 10)
+    cols = (C.c_int64 * 2)(32, 0)
+    cfg = AcpConfig()
+    cfg.abi_version = ACP_ABI_VERSION
+    cfg.num_tensors = 2
+    cfg.rows = C.cast(rows, C.POINTER(C.c_int64))
+    cfg.cols = C.cast(cols, C.POINTER(C.c_int64))
+    cfg.rank = 4
+    cfg.world_size = 2
+    cfg.device = -1
+    ctx = C.c_void_p()
+    assert lib.acp_plan_create(C.byref(cfg), C.byref(ctx)) == 0
+    assert lib.acp_step(ctx, 0, None, None) == ACP_E_STATE
+    assert b"plan-only" in lib.acp_last_error()
+    assert lib.acp_check_finite(ctx, None) == ACP_E_STATE
+    assert lib.acp_get_state(ctx, 0, None, None, None, None) == ACP_E_STATE
+    assert lib.acp_step_begin(ctx, 0, None, None) == ACP_E_STATE
+    assert lib.acp_destroy(ctx) == 0

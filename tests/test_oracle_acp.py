@@ -307,3 +307,80 @@ def test_powersgd_identical_workers():
     for s in range(4):
         g = _grads(shapes, 1, s)
         np.testing.assert_allclose(a.step(g)[0], b.step([g[0], g[0]])[0], atol=1e-12)
+
+
+# -- Power-SGD error feedback (reading C13, Alg. 1 + P:211) ----------------------
+# Alg. 1 prints no error-feedback line; C13 reads it as Alg. 2's:
+# E_w = M'_w - P_hat Q_w^T with the orthogonalised aggregated P_hat and the
+# worker's LOCAL Q_w = M'_w^T P_hat. The pins below are properties of that
+# formula that the alternatives break: E from the aggregated Q (Alg. 2's
+# "before aggregation" violated), SPEC's E = M' - decoded, a dropped
+# E in M', a sign error.
+def _psgd_run(shapes, p, steps, seed=7, ef=True):
+    o = PowerSgdOracle(shapes, rank=3, world_size=p, seed=seed, ef=ef)
+    for s in range(steps):
+        g = _grads(shapes, p, s, seed=seed)
+        Mp = [{i: np.float64(g[w][i]).reshape(o.E[w][i].shape) + o.E[w][i] for i in o.E[w]}
+              for w in range(p)]
+        d = o.step(g)
+        yield o, g, Mp, d
+
+
+def test_powersgd_ef_residual_orthogonal_to_decoded_range():
+    """P_hat^T E_w = P_hat^T M'_w - Q_w^T = 0 for the LOCAL Q_w, so every
+    worker's residual is orthogonal to the range of the decoded gradient
+    (decoded^T E_w = 0). Fails for E from the aggregated Q and for SPEC's
+    E = M' - decoded, whenever the workers' inputs differ."""
+    shapes = [(20, 9)]
+    for o, g, Mp, d in _psgd_run(shapes, 3, 4):
+        D = d[0]
+        for w in range(3):
+            E = o.E[w][0]
+            assert np.abs(D.T @ E).max() <= 1e-12 * np.linalg.norm(D) * np.linalg.norm(Mp[w][0])
+            assert np.linalg.norm(E) > 1e-3  # not trivially zero (r < rank of M')
+    # the alternatives violate it
+    o = PowerSgdOracle(shapes, rank=3, world_size=3, seed=7)
+    g = _grads(shapes, 3, 0, seed=7)
+    d = o.step(g)[0]
+    alt = np.float64(g[1][0]) - d                  # SPEC's E = M' - decoded (p > 1)
+    assert np.abs(d.T @ alt).max() > 1e-3 * np.linalg.norm(d) * np.linalg.norm(alt)
+
+
+def test_powersgd_ef_sum_identity_and_conservation():
+    """Sum over workers: sum_w E_w = sum_w M'_w - p * decoded (because
+    sum_w P_hat Q_w^T = P_hat Q^T = p * decoded). E from the aggregated Q
+    would give sum_w M'_w - p^2 * decoded instead."""
+    p = 3
+    for o, g, Mp, d in _psgd_run([(16, 12), (12,)], p, 4):
+        lhs = sum(o.E[w][0] for w in range(p))
+        rhs = sum(Mp[w][0] for w in range(p)) - p * d[0]
+        assert np.abs(lhs - rhs).max() <= 1e-12 * max(1.0, np.abs(rhs).max())
+        assert np.abs(d[0]).max() > 1e-3
+
+
+def test_powersgd_ef_telescoping_single_worker():
+    """p = 1: E_T = sum_s M_s - sum_s decoded_s -- the
+    compression error is carried, never lost; a dropped E in M' or a sign
+    error breaks it after the second step."""
+    shapes = [(14, 10)]
+    acc_m = np.zeros((14, 10))
+    acc_d = np.zeros((14, 10))
+    for o, g, Mp, d in _psgd_run(shapes, 1, 6):
+        acc_m += np.float64(g[0][0])
+        acc_d += d[0]
+        np.testing.assert_allclose(o.E[0][0], acc_m - acc_d, atol=1e-11)
+
+
+def test_powersgd_ef_feeds_next_step():
+    """M' = M + E: an EF-off oracle fed M + E_prev by hand follows the
+    EF-on trajectory exactly (same Q state, same decoded gradients)."""
+    shapes = [(18, 11)]
+    p = 2
+    a = PowerSgdOracle(shapes, rank=2, world_size=p, seed=9)
+    b = PowerSgdOracle(shapes, rank=2, world_size=p, seed=9, ef=False)
+    for s in range(5):
+        g = _grads(shapes, p, s, seed=9)
+        fed = [[(np.float64(g[w][0]) + a.E[w][0])] for w in range(p)]
+        da = a.step(g)[0]
+        db = b.step(fed)[0]
+        np.testing.assert_allclose(da, db, atol=1e-12)
