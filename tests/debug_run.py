@@ -1,9 +1,9 @@
-"""Tiny end-to-end run of every kernel class for compute-sanitizer
-(tests/test_gpu_sanitizer.py): K2 (CholeskyQR2), the SIMT stream K1 / decode
+"""Tiny end-to-end run of every kernel class (debug builds with device-side
+checks, ACP_LIB=...): K2 (CholeskyQR2), the SIMT stream K1 / decode
 kernels (r = 4, deferred residual; 1-D packing; the generic path), the
 tensor-core kernels (r = 8: K1 P/Q steps, column reduce, decodes), the
 register row/column kernels (NO_EF), state access, for a few alternating
-steps, eagerly and through a captured graph. Prints 'sanitize ok'."""
+steps, eagerly and through a captured graph. Prints 'debug run ok'."""
 import os
 import sys
 
@@ -31,7 +31,7 @@ def main():
             ctx.step(g, 0)
             torch.cuda.synchronize()
             ctx.close()
-    print("sanitize ok")
+    print("debug run ok")
 
 
 if __name__ == "__main__":
