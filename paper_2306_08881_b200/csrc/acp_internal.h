@@ -174,9 +174,12 @@ struct Tables {
   const NvlsArgs* nv;
   FusedSync* fsync;
   int32_t* nonfinite;  // sticky flag: bit 0 K2 saw a non-finite factor, bit 1 finite scan hit
-  int32_t nvls_fused;  // TC path: per layer [M, S, Q_orth hi, lo, Q_loc hi, lo] (P-step
-                             // boxes), [M, S] (Q-step boxes of tq.tr rows), [Q slot]: 9 maps
+  int32_t nvls_fused;
 };
+// TC path TMA maps per layer: [M, S, Q_orth hi, lo, Q_loc hi, lo] (P-step
+// boxes), [M, S] (Q-step boxes of tq.tr rows), [Q slot] (R8-row boxes),
+// [gradient, 32-row boxes] (tcgen05 decode store)
+constexpr int kTmapsPerLayer = 10;
 
 // NVLS all-reduce (k_nvls.cu): the fused buffers live in a
 // symmetric region bound to a multicast object; flags for the cross-rank
@@ -243,6 +246,10 @@ bool stream_make_map(int mode, int64_t m, int rt, StreamMap* out);
 cudaError_t launch_tc(int mode, int r8, const Tables& t, const TcSeg* segs, const int32_t* cta_begin,
                       int ncta, int stages, int stage_floats, float scale, cudaStream_t stream);
 int tc_d_stage_floats(int r8);
+// tcgen05 decodes (k_tc5.cu): mode 2 P-step, mode 3 Q-step; one CTA per SM
+cudaError_t launch_tc5_decode(int mode, int r8, const Tables& t, const TcSeg* segs, const int32_t* cta_begin,
+                              int ncta, float scale, cudaStream_t stream);
+size_t tc5_smem_bytes(int r8);
 size_t tc_smem_bytes(int stages, int stage_floats);
 // host: encode a 2-D TMA map (fp32 rows x cols, 32-column boxes of box_rows
 // rows, SWIZZLE_128B); false (map zeroed) when the layout does not allow it

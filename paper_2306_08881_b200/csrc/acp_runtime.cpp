@@ -63,6 +63,7 @@ struct Plan {
   bool psgd = false;    // ACP_POWERSGD: the Power-SGD baseline (NEXT-1)
   bool tc = false;      // tensor-core K1 + double-deferred residual
   bool bucketed = false;  // multi-rank scheduler (world_size > 1 or ACP_BUCKETED)
+  bool tc5 = false;       // TC path decodes on tcgen05 / TMEM (k_tc5.cu); ACP_NO_TC5=1: mma.sync
   int R8 = 0;           // TC path: rank padded to a multiple of 8
   int64_t qs_elems = 0, ps_elems = 0;  // TC path: split-factor array sizes (floats)
   std::vector<TcSeg> tcsegs;
@@ -204,6 +205,7 @@ acp_status build_plan(const acp_config* cfg, Plan& P, bool plan_only = false) {
   P.tc = P.ef && !P.psgd && P.RT <= 32 && !std::getenv("ACP_NO_TC") &&
          (P.RT >= 8 || (tc_env && std::atoi(tc_env) != 0));
   P.R8 = P.tc ? std::max(8, (P.RT + 7) / 8 * 8) : 0;
+  P.tc5 = P.tc && !std::getenv("ACP_NO_TC5");
   int tc_q_stage = 0;
   // offsets
   int64_t e = 0, ql = 0, w = 0, so[2] = {0, 0}, qs = 0, ps = 0;
@@ -564,11 +566,13 @@ acp_status build_plan(const acp_config* cfg, Plan& P, bool plan_only = false) {
     ln.cb_off = (int64_t)P.ctab.size();
     ln.stage_floats = std::max(4, mode == 0 ? tc_p_stage_floats(P.R8)
                                             : (mode == 1 ? tc_q_stage : tc_d_stage_floats(P.R8)));
-    // decodes run two CTAs per SM (more warps to hide the MMA chains)
-    const int tc_cps = mode >= 2 ? 2 : 1;
+    // mma.sync decodes run two CTAs per SM (more warps to hide the MMA
+    // chains); the tcgen05 decodes one persistent CTA per SM
+    const int tc_cps = (mode >= 2 && !P.tc5) ? 2 : 1;
     ln.stages = (int)std::max<int64_t>(2, std::min<int64_t>(mode >= 2 ? 8 : 6,
                                                             (200 * 1024 / tc_cps) / (4LL * ln.stage_floats)));
     if (tc_smem_bytes(ln.stages, ln.stage_floats) > 227 * 1024) smem_overflow = true;
+    if (mode >= 2 && P.tc5 && tc5_smem_bytes(P.R8) > 227 * 1024) smem_overflow = true;
     int64_t part = 0;
     int prev_layer = -1, prev_panel = -1;
     ln.red_off = (int64_t)P.redtasks.size();
@@ -751,7 +755,7 @@ acp_status build_plan(const acp_config* cfg, Plan& P, bool plan_only = false) {
   P.off_psplit = take(4 * (size_t)P.ps_elems);
   P.off_plsplit = take(4 * (size_t)P.ps_elems);
   P.off_tcsegs = take(sizeof(TcSeg) * P.tcsegs.size());
-  P.off_tmaps = take(P.tc ? sizeof(CUtensorMap) * 9 * (size_t)P.T : 0);
+  P.off_tmaps = take(P.tc ? sizeof(CUtensorMap) * kTmapsPerLayer * (size_t)P.T : 0);
   P.off_nvargs = take(sizeof(NvlsArgs));
   P.off_fsync = take(2 * sizeof(FusedSync));
   P.off_nvepoch = take(4 * (size_t)kNvlsMaxCtas);
@@ -915,7 +919,9 @@ acp_status run_k3(acp_ctx* c, int parity, const Launch& ln, cudaStream_t s, bool
   tt.nvls_fused = fused ? 1 : 0;  // this decode first sums its buffer over the ranks (NVLS)
   ProfRec* r = prof_begin(c, parity == 0 ? ACP_K_DECODE_P : ACP_K_DECODE_Q, ln.bytes, s);
   cudaError_t e =
-      ln.kind == 3
+      (ln.kind == 3 && c->P.tc5)
+          ? launch_tc5_decode(ln.mode, c->P.R8, tt, dev_tcsegs(c, ln), dev_ctab(c, ln), ln.ncta, decode_scale(c), s)
+      : ln.kind == 3
           ? launch_tc(ln.mode, c->P.R8, tt, dev_tcsegs(c, ln), dev_ctab(c, ln), ln.ncta, ln.stages,
                       ln.stage_floats, decode_scale(c), s)
       : ln.kind == 2
@@ -963,12 +969,12 @@ acp_status set_grads(acp_ctx* c, float* const* grads, cudaStream_t s) {
   if (c->P.tc) {
     // TC P-step: TMA maps of the gradients (M) next to the fixed ones (S, factors)
     const Plan& P = c->P;
-    c->tmaps.resize(9 * (size_t)P.T);
+    c->tmaps.resize(kTmapsPerLayer * (size_t)P.T);
     for (int i = 0; i < P.T; ++i) {
       const LayerDesc& L = P.L[i];
-      CUtensorMap* mp = c->tmaps.data() + 9 * (size_t)i;
+      CUtensorMap* mp = c->tmaps.data() + kTmapsPerLayer * (size_t)i;
       if (!L.mat) {
-        std::memset(mp, 0, 9 * sizeof(CUtensorMap));
+        std::memset(mp, 0, kTmapsPerLayer * sizeof(CUtensorMap));
         continue;
       }
       const int br = tc_p_box_rows();
@@ -981,6 +987,7 @@ acp_status set_grads(acp_ctx* c, float* const* grads, cudaStream_t s) {
       tc_encode_map(mp + 6, c->grads_cache[i], L.m, L.n, L.tq.tr);
       tc_encode_map(mp + 7, c->tab.E + L.e_off, L.m, L.n, L.tq.tr);
       tc_encode_map(mp + 8, c->tab.qbuf + L.q_off, L.m, L.r, P.R8);
+      tc_encode_map(mp + 9, c->grads_cache[i], L.m, L.n, 32);
     }
     CK(c, cudaMemcpyAsync(c->ws + P.off_tmaps, c->tmaps.data(), sizeof(CUtensorMap) * c->tmaps.size(),
                           cudaMemcpyHostToDevice, s), "tensor map upload");

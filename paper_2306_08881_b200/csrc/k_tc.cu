@@ -129,7 +129,7 @@ __device__ void tcp_producer(const Tables& t, const TcSeg* segs, int sb, int se,
     const float* grad = t.grads[s.layer];
     const float* S = t.E + L.e_off;
     const bool v16 = (m % 4 == 0) && ((reinterpret_cast<uintptr_t>(grad) & 15u) == 0);
-    const CUtensorMap* maps = t.tmaps + 9 * (int64_t)s.layer;  // M, S, Q_orth hi/lo, Q_loc hi/lo
+    const CUtensorMap* maps = t.tmaps + kTmapsPerLayer * (int64_t)s.layer;  // M, S, Q_orth hi/lo, Q_loc hi/lo
     if (v16 && lane < 6) tmap_acquire(maps + lane);
     const float* fq[4] = {t.qsplit + L.qs_off, t.qsplit + L.qs_off + (int64_t)R8 * m,
                           t.qlsplit + L.qs_off, t.qlsplit + L.qs_off + (int64_t)R8 * m};
@@ -389,7 +389,7 @@ __device__ void tcq_producer(const Tables& t, const TcSeg* segs, int sb, int se,
     const int nbox = q_nbox(mp.pc);
     const int tr = mp.tr;
     const bool v16 = (m % 4 == 0) && ((reinterpret_cast<uintptr_t>(grad) & 15u) == 0);
-    const CUtensorMap* maps = t.tmaps + 9 * (int64_t)s.layer + 6;  // M, S with tr-row boxes
+    const CUtensorMap* maps = t.tmaps + kTmapsPerLayer * (int64_t)s.layer + 6;  // M, S with tr-row boxes
     if (v16 && lane < 2) tmap_acquire(maps + lane);
     const float* fr[4] = {t.plsplit + L.ps_off, t.plsplit + L.ps_off + n * R8,
                           t.psplit + L.ps_off, t.psplit + L.ps_off + n * R8};
@@ -476,7 +476,7 @@ __device__ void tcq_consumer(const Tables& t, const TcSeg* segs, int sb, int se,
     // S is written back through shared memory + TMA store (map 7) when rows
     // are 16-byte aligned; otherwise each lane stores its own elements
     const bool tst = (m % 4 == 0);
-    const CUtensorMap* smap = t.tmaps + 9 * (int64_t)s.layer + 7;
+    const CUtensorMap* smap = t.tmaps + kTmapsPerLayer * (int64_t)s.layer + 7;
     // this warp's column blocks (16 columns each) inside the panel
     uint32_t ah[CBW][KB][4], al[CBW][KB][4];
     float acc[CBW][KB][4];
@@ -683,7 +683,7 @@ __device__ void tcd_producer(const Tables& t, const TcSeg* segs, int sb, int se,
     const LayerDesc& L = t.layers[s.layer];
     if (!L.mat) continue;
     const int64_t m = L.m;
-    const CUtensorMap* maps = t.tmaps + 9 * (int64_t)s.layer;
+    const CUtensorMap* maps = t.tmaps + kTmapsPerLayer * (int64_t)s.layer;
     const bool v16 = (m % 4 == 0);
     if (v16 && lane < 9) tmap_acquire(maps + lane);
     const float* src0 = MODE == 2 ? t.qsplit + L.qs_off : t.qbuf + L.q_off;
