@@ -178,8 +178,9 @@ struct Tables {
 };
 // TC path TMA maps per layer: [M, S, Q_orth hi, lo, Q_loc hi, lo] (P-step
 // boxes), [M, S] (Q-step boxes of tq.tr rows), [Q slot] (R8-row boxes),
-// [gradient, 32-row boxes] (tcgen05 decode store)
-constexpr int kTmapsPerLayer = 10;
+// [gradient, 32-row boxes] (tcgen05 decode store), and for the tcgen05
+// decode's column factor (32-byte-atom swizzle): [Q_orth hi, lo, Q slot]
+constexpr int kTmapsPerLayer = 13;
 
 // NVLS all-reduce (k_nvls.cu): the fused buffers live in a
 // symmetric region bound to a multicast object; flags for the cross-rank
@@ -253,7 +254,8 @@ size_t tc5_smem_bytes(int r8);
 size_t tc_smem_bytes(int stages, int stage_floats);
 // host: encode a 2-D TMA map (fp32 rows x cols, 32-column boxes of box_rows
 // rows, SWIZZLE_128B); false (map zeroed) when the layout does not allow it
-bool tc_encode_map(CUtensorMap* out, const float* base, int64_t cols, int64_t rows, int box_rows);
+bool tc_encode_map(CUtensorMap* out, const float* base, int64_t cols, int64_t rows, int box_rows,
+                   bool atom32 = false);
 int tc_p_box_rows();
 int tc_p_stage_floats(int r8);
 // K1 Q-step tile geometry of an m-column layer; returns stage floats

@@ -545,7 +545,14 @@ acp_status build_plan(const acp_config* cfg, Plan& P, bool plan_only = false) {
       }
       if (mode >= 2) {  // decode: grad written (+ the two factors once)
         bytes += 4.0 * (double)L.n * (double)L.m + 4.0 * L.r * (double)(L.n + L.m);
-        units.push_back({i, -1, L.n, 4.0 * (double)L.m * (L.m % 4 ? 6.0 : 1.0), 128});
+        if (P.tc5) {
+          // tcgen05 decode: the unit is a 128-row block, whose time is set by
+          // its 128 x 128 tiles (a partial block costs a whole one)
+          const double mpad = (double)((L.m + 127) / 128 * 128);
+          units.push_back({i, -1, (L.n + 127) / 128, 512.0 * mpad * (L.m % 4 ? 6.0 : 1.0), 1});
+        } else {
+          units.push_back({i, -1, L.n, 4.0 * (double)L.m * (L.m % 4 ? 6.0 : 1.0), 128});
+        }
         continue;
       }
       // algorithmic bytes: M, S read, S written + the factors once
@@ -582,6 +589,10 @@ acp_status build_plan(const acp_config* cfg, Plan& P, bool plan_only = false) {
       sg.layer = u.layer;
       sg.row0 = a;
       sg.row1 = b;
+      if (mode >= 2 && P.tc5 && P.L[u.layer].mat) {  // 128-row block units -> rows
+        sg.row0 = a * 128;
+        sg.row1 = std::min<int64_t>(b * 128, P.L[u.layer].n);
+      }
       sg.panel = u.panel < 0 ? 0 : u.panel;
       const LayerDesc& L = P.L[u.layer];
       if (mode == 1 && L.mat) {
@@ -988,6 +999,9 @@ acp_status set_grads(acp_ctx* c, float* const* grads, cudaStream_t s) {
       tc_encode_map(mp + 7, c->tab.E + L.e_off, L.m, L.n, L.tq.tr);
       tc_encode_map(mp + 8, c->tab.qbuf + L.q_off, L.m, L.r, P.R8);
       tc_encode_map(mp + 9, c->grads_cache[i], L.m, L.n, 32);
+      tc_encode_map(mp + 10, c->tab.qsplit + L.qs_off, L.m, P.R8, P.R8, true);
+      tc_encode_map(mp + 11, c->tab.qsplit + L.qs_off + (int64_t)P.R8 * L.m, L.m, P.R8, P.R8, true);
+      tc_encode_map(mp + 12, c->tab.qbuf + L.q_off, L.m, L.r, P.R8, true);
     }
     CK(c, cudaMemcpyAsync(c->ws + P.off_tmaps, c->tmaps.data(), sizeof(CUtensorMap) * c->tmaps.size(),
                           cudaMemcpyHostToDevice, s), "tensor map upload");

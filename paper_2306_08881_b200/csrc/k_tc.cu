@@ -1002,7 +1002,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
   return fn;
 }
 
-bool tc_encode_map(CUtensorMap* out, const float* base, int64_t cols, int64_t rows, int box_rows) {
+bool tc_encode_map(CUtensorMap* out, const float* base, int64_t cols, int64_t rows, int box_rows, bool atom32) {
   std::memset(out, 0, sizeof(CUtensorMap));
   auto enc = tmap_encoder();
   if (!enc || !base || cols % 4 != 0 || (reinterpret_cast<uintptr_t>(base) & 15u) != 0) return false;
@@ -1011,7 +1011,8 @@ bool tc_encode_map(CUtensorMap* out, const float* base, int64_t cols, int64_t ro
   const cuuint32_t box[2] = {(cuuint32_t)kPBC, (cuuint32_t)box_rows};
   const cuuint32_t estr[2] = {1, 1};
   return enc(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, atom32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 int tc_p_box_rows() { return kPTR; }
