@@ -178,7 +178,7 @@ struct Tables {
 };
 // TC path TMA maps per layer: [M, S, Q_orth hi, lo, Q_loc hi, lo] (P-step
 // boxes), [M, S] (Q-step boxes of tq.tr rows), [Q slot] (R8-row boxes),
-// [gradient, 32-row boxes] (tcgen05 decode store), and for the tcgen05
+// [unused], and for the tcgen05
 // decode's column factor (32-byte-atom swizzle): [Q_orth hi, lo, Q slot]
 constexpr int kTmapsPerLayer = 13;
 
@@ -248,7 +248,9 @@ cudaError_t launch_tc(int mode, int r8, const Tables& t, const TcSeg* segs, cons
                       int ncta, int stages, int stage_floats, float scale, cudaStream_t stream);
 int tc_d_stage_floats(int r8);
 // tcgen05 decodes (k_tc5.cu): mode 2 P-step, mode 3 Q-step; one CTA per SM
-cudaError_t launch_tc5_decode(int mode, int r8, const Tables& t, const TcSeg* segs, const int32_t* cta_begin,
+// (items: 128-row blocks / vector chunks fetched dynamically through the
+// counter pair `sched`, which must start at {0, 0}; the kernel re-arms it)
+cudaError_t launch_tc5_decode(int mode, int r8, const Tables& t, const TcSeg* items, int nitems, int32_t* sched,
                               int ncta, float scale, cudaStream_t stream);
 size_t tc5_smem_bytes(int r8);
 size_t tc_smem_bytes(int stages, int stage_floats);

@@ -98,7 +98,7 @@ struct Plan {
          off_grads = 0, off_rowsegs = 0, off_colsegs = 0, off_streamsegs = 0, off_orth[2] = {0, 0},
          off_ctab = 0, off_step = 0, off_red = 0, off_defer = 0,
          off_qsplit = 0, off_qlsplit = 0, off_psplit = 0, off_plsplit = 0, off_tcsegs = 0,
-         off_tmaps = 0, off_nvargs = 0, off_fsync = 0, off_nvepoch = 0, off_nonfinite = 0,
+         off_tmaps = 0, off_nvargs = 0, off_fsync = 0, off_nvepoch = 0, off_nonfinite = 0, off_tc5sched = 0,
          total = 0;
 };
 
@@ -534,6 +534,38 @@ acp_status build_plan(const acp_config* cfg, Plan& P, bool plan_only = false) {
     return fail(ACP_E_INVAL, "ACP_POWERSGD needs error feedback and rank <= 8");
   // tensor-core K1 launch (mode 0 P-step, 1 Q-step) over `tensors`
   auto tc_launch = [&](int mode, const std::vector<int>& tensors) {
+    if (mode >= 2 && P.tc5) {
+      // tcgen05 decode (k_tc5.cu): a flat list of work items fetched
+      // dynamically by one persistent CTA per SM -- 128-row blocks of every
+      // matrix, largest layers (most tiles per block) first, then chunks of
+      // the 1-D tensors
+      Launch ln;
+      ln.kind = 3;
+      ln.mode = mode;
+      ln.seg_off = (int64_t)P.tcsegs.size();
+      std::vector<int> order(tensors);
+      std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+        const LayerDesc &A = P.L[a], &B = P.L[b];
+        if (A.mat != B.mat) return A.mat > B.mat;
+        return A.m > B.m;
+      });
+      for (int i : order) {
+        const LayerDesc& L = P.L[i];
+        const int64_t step = L.mat ? 128 : 32768;
+        for (int64_t r0 = 0; r0 < L.n; r0 += step) {
+          TcSeg sg{};
+          sg.layer = i;
+          sg.row0 = r0;
+          sg.row1 = std::min<int64_t>(L.n, r0 + step);
+          P.tcsegs.push_back(sg);
+        }
+        ln.bytes += L.mat ? 4.0 * (double)L.n * (double)L.m + 4.0 * L.r * (double)(L.n + L.m) : 8.0 * L.n;
+      }
+      ln.nitems = (int)((int64_t)P.tcsegs.size() - ln.seg_off);
+      ln.ncta = std::min(nsm, std::max(1, ln.nitems));
+      if (tc5_smem_bytes(P.R8) > 227 * 1024) smem_overflow = true;
+      return ln;
+    }
     std::vector<Unit> units;
     double bytes = 0;
     for (int i : tensors) {
@@ -545,14 +577,7 @@ acp_status build_plan(const acp_config* cfg, Plan& P, bool plan_only = false) {
       }
       if (mode >= 2) {  // decode: grad written (+ the two factors once)
         bytes += 4.0 * (double)L.n * (double)L.m + 4.0 * L.r * (double)(L.n + L.m);
-        if (P.tc5) {
-          // tcgen05 decode: the unit is a 128-row block, whose time is set by
-          // its 128 x 128 tiles (a partial block costs a whole one)
-          const double mpad = (double)((L.m + 127) / 128 * 128);
-          units.push_back({i, -1, (L.n + 127) / 128, 512.0 * mpad * (L.m % 4 ? 6.0 : 1.0), 1});
-        } else {
-          units.push_back({i, -1, L.n, 4.0 * (double)L.m * (L.m % 4 ? 6.0 : 1.0), 128});
-        }
+        units.push_back({i, -1, L.n, 4.0 * (double)L.m * (L.m % 4 ? 6.0 : 1.0), 128});
         continue;
       }
       // algorithmic bytes: M, S read, S written + the factors once
@@ -579,7 +604,6 @@ acp_status build_plan(const acp_config* cfg, Plan& P, bool plan_only = false) {
     ln.stages = (int)std::max<int64_t>(2, std::min<int64_t>(mode >= 2 ? 8 : 6,
                                                             (200 * 1024 / tc_cps) / (4LL * ln.stage_floats)));
     if (tc_smem_bytes(ln.stages, ln.stage_floats) > 227 * 1024) smem_overflow = true;
-    if (mode >= 2 && P.tc5 && tc5_smem_bytes(P.R8) > 227 * 1024) smem_overflow = true;
     int64_t part = 0;
     int prev_layer = -1, prev_panel = -1;
     ln.red_off = (int64_t)P.redtasks.size();
@@ -589,10 +613,7 @@ acp_status build_plan(const acp_config* cfg, Plan& P, bool plan_only = false) {
       sg.layer = u.layer;
       sg.row0 = a;
       sg.row1 = b;
-      if (mode >= 2 && P.tc5 && P.L[u.layer].mat) {  // 128-row block units -> rows
-        sg.row0 = a * 128;
-        sg.row1 = std::min<int64_t>(b * 128, P.L[u.layer].n);
-      }
+
       sg.panel = u.panel < 0 ? 0 : u.panel;
       const LayerDesc& L = P.L[u.layer];
       if (mode == 1 && L.mat) {
@@ -771,6 +792,7 @@ acp_status build_plan(const acp_config* cfg, Plan& P, bool plan_only = false) {
   P.off_fsync = take(2 * sizeof(FusedSync));
   P.off_nvepoch = take(4 * (size_t)kNvlsMaxCtas);
   P.off_nonfinite = take(4);
+  P.off_tc5sched = take(4 * 4);  // tcgen05 decodes: [item counter, exited CTAs] per parity
   P.off_step = take(8);
   P.off_defer = take(8);
   P.off_red = take(sizeof(ColReduceTask) * P.redtasks.size());
@@ -931,7 +953,9 @@ acp_status run_k3(acp_ctx* c, int parity, const Launch& ln, cudaStream_t s, bool
   ProfRec* r = prof_begin(c, parity == 0 ? ACP_K_DECODE_P : ACP_K_DECODE_Q, ln.bytes, s);
   cudaError_t e =
       (ln.kind == 3 && c->P.tc5)
-          ? launch_tc5_decode(ln.mode, c->P.R8, tt, dev_tcsegs(c, ln), dev_ctab(c, ln), ln.ncta, decode_scale(c), s)
+          ? launch_tc5_decode(ln.mode, c->P.R8, tt, dev_tcsegs(c, ln), ln.nitems,
+                              reinterpret_cast<int32_t*>(c->ws + c->P.off_tc5sched) + 2 * (ln.mode - 2), ln.ncta,
+                              decode_scale(c), s)
       : ln.kind == 3
           ? launch_tc(ln.mode, c->P.R8, tt, dev_tcsegs(c, ln), dev_ctab(c, ln), ln.ncta, ln.stages,
                       ln.stage_floats, decode_scale(c), s)
@@ -998,7 +1022,6 @@ acp_status set_grads(acp_ctx* c, float* const* grads, cudaStream_t s) {
       tc_encode_map(mp + 6, c->grads_cache[i], L.m, L.n, L.tq.tr);
       tc_encode_map(mp + 7, c->tab.E + L.e_off, L.m, L.n, L.tq.tr);
       tc_encode_map(mp + 8, c->tab.qbuf + L.q_off, L.m, L.r, P.R8);
-      tc_encode_map(mp + 9, c->grads_cache[i], L.m, L.n, 32);
       tc_encode_map(mp + 10, c->tab.qsplit + L.qs_off, L.m, P.R8, P.R8, true);
       tc_encode_map(mp + 11, c->tab.qsplit + L.qs_off + (int64_t)P.R8 * L.m, L.m, P.R8, P.R8, true);
       tc_encode_map(mp + 12, c->tab.qbuf + L.q_off, L.m, L.r, P.R8, true);
