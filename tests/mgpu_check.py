@@ -41,9 +41,14 @@ def main():
     # paper rule, one tensor per bucket, one bucket; the Power-SGD baseline;
     # then the NVLS all-reduce (symmetric memory) with the paper rule and the
     # bucket API
-    runs = [(25 * 2 ** 20, 0, False), (0, 0, False), (-1, 0, False), (25 * 2 ** 20, ACP_POWERSGD, False),
-            (25 * 2 ** 20, 0, True), (0, 0, True)]
-    for bucket_bytes, flags, nvls in runs:
+    # ... and the tensor-core path (rank 8: tcgen05 decodes) with NCCL and
+    # with the NVLS reduction fused into the tcgen05 decode's prologue
+    runs = [(25 * 2 ** 20, 0, False, 4), (0, 0, False, 4), (-1, 0, False, 4),
+            (25 * 2 ** 20, ACP_POWERSGD, False, 4), (25 * 2 ** 20, 0, True, 4), (0, 0, True, 4),
+            (25 * 2 ** 20, 0, False, 8), (25 * 2 ** 20, 0, True, 8)]
+    q0s = {4: q0, 8: make_q0(shapes, 8, seed)}
+    for bucket_bytes, flags, nvls, rank_r in runs:
+        q0 = q0s[rank_r]
         ctx = AcpContext(shapes, rank_r, world_size=world, nccl_comm=comm, seed=seed, q0=q0,
                          bucket_bytes=bucket_bytes, flags=flags)
         if nvls and not ctx.attach_symmetric():
@@ -53,7 +58,7 @@ def main():
             continue
         oc = PowerSgdOracle if flags else AcpOracle
         if rank == 0:
-            print(f"run bucket_bytes={bucket_bytes} flags={flags} nvls={nvls}", flush=True)
+            print(f"run rank={rank_r} bucket_bytes={bucket_bytes} flags={flags} nvls={nvls}", flush=True)
         o = oc(shapes, rank_r, world_size=world, seed=seed, q0=q0)
         for t in range(steps):
             g = [torch.from_numpy(np.ascontiguousarray(x)).cuda() for x in inputs[t][rank]]
