@@ -32,6 +32,87 @@ constexpr size_t orth_smem() {
 // (set by the layer's last segment of the previous phase).
 __device__ __forceinline__ long long orth_epoch(int64_t step, int phase) { return step * 4 + phase; }
 
+// Cholesky G = R^T R (R upper) and W = R^-1 of one layer's r x r Gram by one
+// warp, with lane l holding column l in registers (RT >= 16; the smem-based
+// left-looking version below serialises ~r^2 dependent shared-memory round
+// trips, ~20 us at r = 32). Right-looking: at step k the pivot comes from
+// lane k by a shuffle, every lane forms its entry of row k of R, and the
+// trailing columns are updated with row k broadcast lane by lane. Reading C6
+// as in the smem version: a column whose Schur pivot is <= 1e-12 of its
+// squared norm (or whose norm is 0) is dropped (row and column of R zero,
+// R_kk = 1, W_kk = 0); a non-finite diagonal raises the sticky flag and is
+// not repaired. W = R^-1 column by column in registers (lane l:
+// back substitution, R rows read from shared memory).
+template <int RT>
+__device__ __noinline__ void chol_inv_regs(const Tables& t, const LayerDesc& L, const double* Gs, double* Rm,
+                                           double* Wout, int r, int phase, int64_t step) {
+  const int l = threadIdx.x & 31;
+  double a[RT];  // column l of the (Schur-updated) Gram
+#pragma unroll
+  for (int i = 0; i < RT; ++i) a[i] = (i < r && l < r) ? Gs[i * r + l] : 0.0;
+  bool mydg = false, nonfinite = false;
+#pragma unroll
+  for (int k = 0; k < RT; ++k) {
+    if (k >= r) break;
+    const double dkk = __shfl_sync(0xffffffffu, a[k], k);  // Schur pivot G'[k][k]
+    const double gkk = Gs[k * r + k];                      // squared norm of column k
+    const bool fin = isfinite(gkk);
+    nonfinite |= !fin;
+    const bool dg = fin && (!(gkk > 0.0) || !(dkk > kDegTol2 * gkk));
+    const double rkk = dg ? 1.0 : sqrt(dkk);
+    double rkl = 0.0;  // R[k][l]
+    if (l == k) {
+      rkl = rkk;
+      mydg = dg;
+    } else if (l > k && l < r) {
+      rkl = dg ? 0.0 : a[k] / rkk;
+    }
+    if (l >= k && l < r) Rm[k * r + l] = rkl;
+    if (dg && l < k) Rm[l * r + k] = 0.0;  // a dropped column has no entries above R_kk
+#pragma unroll
+    for (int i = k + 1; i < RT; ++i) {
+      const double rki = __shfl_sync(0xffffffffu, rkl, i);
+      if (l > k) a[i] = fma(-rki, rkl, a[i]);
+    }
+  }
+  __syncwarp();
+  // W = R^-1, column l: w[i] = (delta_il - sum_{i<j<=l} R[i][j] w[j]) / R[i][i]
+  double w[RT];
+#pragma unroll
+  for (int i = RT - 1; i >= 0; --i) {
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int j = i + 1; j < RT; ++j) {
+      if (j <= l && j < r) {
+        if ((j - i) & 1) s0 = fma(Rm[i * r + j], w[j], s0);
+        else s1 = fma(Rm[i * r + j], w[j], s1);
+      }
+    }
+    w[i] = 0.0;
+    if (i < r && i <= l && l < r) {
+      const double rii = Rm[i * r + i];
+      // a dropped column l: W_ll = 0 (its output column is replaced by the
+      // seeded one); its entries above are 0 either way, since R_il = 0
+      w[i] = (i == l) ? (mydg ? 0.0 : 1.0 / rii) : -(s0 + s1) / rii;
+    }
+  }
+  if (l < r) {
+#pragma unroll
+    for (int i = 0; i < RT; ++i)
+      if (i < r) Wout[i * r + l] = (i <= l) ? w[i] : 0.0;
+  }
+  const uint32_t dmask = __ballot_sync(0xffffffffu, mydg && l < r);
+  const bool anynf = __any_sync(0xffffffffu, nonfinite);
+  if (l == 0) {
+    if (anynf) atomicOr(t.nonfinite, 1);
+    if (phase == 0) t.degmask[L.deg_idx] = dmask;
+    t.orthcnt[L.deg_idx] = 0;  // re-arm
+    __threadfence();
+    // publish: the layer's next phase may start
+    *reinterpret_cast<volatile long long*>(t.orthflag + L.deg_idx) = orth_epoch(step, phase + 1);
+  }
+}
+
 // One (phase, segment) work item of K2. Returns after the item; the layer's
 // last segment of phases 0 / 1 also computes W1 / W2 and publishes the
 // layer's next phase through lflag.
@@ -136,7 +217,40 @@ __device__ void orth_item(const Tables& t, int side, const OrthSeg& s, int phase
   const int S = NP <= kThreads ? kThreads / NP : 1;
   const int sp = NP <= kThreads ? tid % S : 0;
   double* part = t.gram + s.gram_off;
-  if (NP <= kThreads) {
+  if constexpr (RT >= 16) {
+    // 2 x 2 register blocks over the full RT x RT Gram (RT = 32: one block
+    // per thread; RT = 16: four row splits per block, summed by shuffles):
+    // 4 DFMA per 4 shared loads, four independent accumulation chains
+    constexpr int BPR = RT / 2, NB = BPR * BPR, SB = kThreads / NB;
+    const int bk = (tid / SB) / BPR, bl = (tid / SB) % BPR, ss = tid % SB;
+    const int k0 = 2 * bk, l0 = 2 * bl;
+    const bool ok0 = k0 < r, ok1 = k0 + 1 < r, ol0 = l0 < r, ol1 = l0 + 1 < r;
+    const float* gk0 = G + (ok0 ? k0 : 0) * kLd;
+    const float* gk1 = G + (ok1 ? k0 + 1 : 0) * kLd;
+    const float* gl0 = G + (ol0 ? l0 : 0) * kLd;
+    const float* gl1 = G + (ol1 ? l0 + 1 : 0) * kLd;
+    double c00 = 0.0, c01 = 0.0, c10 = 0.0, c11 = 0.0;
+    for (int i = ss; i < nr; i += SB) {
+      const double a0 = gk0[i], a1 = gk1[i], b0 = gl0[i], b1 = gl1[i];
+      c00 = fma(a0, b0, c00);
+      c01 = fma(a0, b1, c01);
+      c10 = fma(a1, b0, c10);
+      c11 = fma(a1, b1, c11);
+    }
+#pragma unroll
+    for (int off = SB / 2; off > 0; off >>= 1) {
+      c00 += __shfl_down_sync(0xffffffffu, c00, off, SB);
+      c01 += __shfl_down_sync(0xffffffffu, c01, off, SB);
+      c10 += __shfl_down_sync(0xffffffffu, c10, off, SB);
+      c11 += __shfl_down_sync(0xffffffffu, c11, off, SB);
+    }
+    if (ss == 0) {
+      if (ok0 && ol0) part[k0 * r + l0] = c00;
+      if (ok0 && ol1) part[k0 * r + l0 + 1] = c01;
+      if (ok1 && ol0) part[(k0 + 1) * r + l0] = c10;
+      if (ok1 && ol1) part[(k0 + 1) * r + l0 + 1] = c11;
+    }
+  } else if (NP <= kThreads) {
     const int pi = tid / S;
     double a = 0.0;
     int k = 0, l = 0;
@@ -185,7 +299,9 @@ __device__ void orth_item(const Tables& t, int side, const OrthSeg& s, int phase
     Rm[idx] = 0.0;
   }
   __syncthreads();
-  if (tid < 32) {
+  if constexpr (RT >= 16) {
+    if (tid < 32) chol_inv_regs<RT>(t, L, Gs, Rm, phase == 0 ? W1 : W2, r, phase, step);
+  } else if (tid < 32) {
     const int lane = tid;
     uint32_t dmask = 0;
     bool nonfinite = false;
