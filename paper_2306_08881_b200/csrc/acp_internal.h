@@ -178,9 +178,11 @@ struct Tables {
 };
 // TC path TMA maps per layer: [M, S, Q_orth hi, lo, Q_loc hi, lo] (P-step
 // boxes), [M, S] (Q-step boxes of tq.tr rows), [Q slot] (R8-row boxes),
-// [unused], and for the tcgen05
-// decode's column factor (32-byte-atom swizzle): [Q_orth hi, lo, Q slot]
-constexpr int kTmapsPerLayer = 13;
+// [unused], for the tcgen05 decode's column factor (32-byte-atom swizzle)
+// [Q_orth hi, lo, Q slot] (10-12), and for the tcgen05 K1 P-step [Q_loc hi,
+// lo] (32-byte-atom swizzle, 13-14) and [P_orth hi, lo] (R8 x 128-row boxes,
+// swizzle = R8 * 4 bytes, 15-16)
+constexpr int kTmapsPerLayer = 17;
 
 // NVLS all-reduce (k_nvls.cu): the fused buffers live in a
 // symmetric region bound to a multicast object; flags for the cross-rank
@@ -253,11 +255,16 @@ int tc_d_stage_floats(int r8);
 cudaError_t launch_tc5_decode(int mode, int r8, const Tables& t, const TcSeg* items, int nitems, int32_t* sched,
                               int ncta, float scale, cudaStream_t stream);
 size_t tc5_smem_bytes(int r8);
+// tcgen05 K1 P-step (k_tc5k1.cu): items = 128-row blocks of layers with
+// m % 4 == 0 and 16-byte-aligned gradients, and 1-D tensor chunks
+cudaError_t launch_tc5_k1p(int r8, const Tables& t, const TcSeg* items, int nitems, int32_t* sched, int ncta,
+                           cudaStream_t stream);
+size_t tc5_k1p_smem_bytes(int r8);
 size_t tc_smem_bytes(int stages, int stage_floats);
 // host: encode a 2-D TMA map (fp32 rows x cols, 32-column boxes of box_rows
 // rows, SWIZZLE_128B); false (map zeroed) when the layout does not allow it
 bool tc_encode_map(CUtensorMap* out, const float* base, int64_t cols, int64_t rows, int box_rows,
-                   bool atom32 = false);
+                   bool atom32 = false, int box_cols = 32);
 int tc_p_box_rows();
 int tc_p_stage_floats(int r8);
 // K1 Q-step tile geometry of an m-column layer; returns stage floats

@@ -80,6 +80,11 @@ struct Plan {
   std::vector<OrthSeg> orthsegs[2];
   std::vector<int32_t> ctab;
   Launch k1_all[2], k3_all[2];
+  // tcgen05 K1 P-step (k_tc5k1.cu): items of the TMA-able layers (+ vectors),
+  // and a mma.sync launch for the matrices with m % 4 != 0; used when every
+  // such layer's gradient is 16-byte aligned (acp_ctx::tc5k1_ok), else k1_all
+  bool tc5k1 = false;
+  Launch k1_t5, k1_t5rest;
   Launch k3_fused[2];  // decodes planned as one resident wave (NVLS-fused prologue)
   // world_size > 1: compute groups = runs of consecutive buckets whose
   // projection / decode run as one launch; each bucket is still its own
@@ -206,6 +211,7 @@ acp_status build_plan(const acp_config* cfg, Plan& P, bool plan_only = false) {
          (P.RT >= 8 || (tc_env && std::atoi(tc_env) != 0));
   P.R8 = P.tc ? std::max(8, (P.RT + 7) / 8 * 8) : 0;
   P.tc5 = P.tc && !std::getenv("ACP_NO_TC5");
+  P.tc5k1 = P.tc5 && !std::getenv("ACP_NO_TC5K1");
   int tc_q_stage = 0;
   // offsets
   int64_t e = 0, ql = 0, w = 0, so[2] = {0, 0}, qs = 0, ps = 0;
@@ -667,6 +673,40 @@ acp_status build_plan(const acp_config* cfg, Plan& P, bool plan_only = false) {
   for (int i = 0; i < P.T; ++i) all[i] = i;
   for (int p = 0; p < 2; ++p) {
     P.k1_all[p] = k1_launch(p, all);
+    if (p == 0 && P.tc5k1) {
+      // tcgen05 P-step: 128-row blocks of every matrix with m % 4 == 0
+      // (largest rows first), then vector chunks; the rest via mma.sync
+      std::vector<int> rest, mats;
+      for (int i : all)
+        if (P.L[i].mat && P.L[i].m % 4 != 0) rest.push_back(i);
+        else mats.push_back(i);
+      std::stable_sort(mats.begin(), mats.end(), [&](int a, int b) {
+        const LayerDesc &A = P.L[a], &B = P.L[b];
+        if (A.mat != B.mat) return A.mat > B.mat;
+        return A.m > B.m;
+      });
+      Launch ln;
+      ln.kind = 5;
+      ln.mode = 0;
+      ln.seg_off = (int64_t)P.tcsegs.size();
+      for (int i : mats) {
+        const LayerDesc& L = P.L[i];
+        const int64_t step = L.mat ? 128 : 32768;
+        for (int64_t r0 = 0; r0 < L.n; r0 += step) {
+          TcSeg sg{};
+          sg.layer = i;
+          sg.row0 = r0;
+          sg.row1 = std::min<int64_t>(L.n, r0 + step);
+          P.tcsegs.push_back(sg);
+        }
+        ln.bytes += L.mat ? 12.0 * (double)L.n * (double)L.m + 4.0 * L.r * (2.0 * L.n + 2.0 * L.m) : 8.0 * L.n;
+      }
+      ln.nitems = (int)((int64_t)P.tcsegs.size() - ln.seg_off);
+      ln.ncta = std::min(nsm, std::max(1, ln.nitems));
+      if (tc5_k1p_smem_bytes(P.R8) > 227 * 1024) smem_overflow = true;
+      P.k1_t5 = ln;
+      if (!rest.empty()) P.k1_t5rest = k1_launch(0, rest);
+    }
     P.k3_all[p] = k3_launch(p, all);
   }
   if (cfg->world_size > 1) {  // decode variants for the NVLS-fused prologue
@@ -792,7 +832,9 @@ acp_status build_plan(const acp_config* cfg, Plan& P, bool plan_only = false) {
   P.off_fsync = take(2 * sizeof(FusedSync));
   P.off_nvepoch = take(4 * (size_t)kNvlsMaxCtas);
   P.off_nonfinite = take(4);
-  P.off_tc5sched = take(4 * 4);  // tcgen05 decodes: [item counter, exited CTAs] per parity
+  // tcgen05 kernels' dynamic item counters [next item, exited CTAs]: decode P,
+  // decode Q, K1 P-step, K1 Q-step
+  P.off_tc5sched = take(4 * 8);
   P.off_step = take(8);
   P.off_defer = take(8);
   P.off_red = take(sizeof(ColReduceTask) * P.redtasks.size());
@@ -843,6 +885,7 @@ struct acp_ctx {
   int64_t sym_q_off = 0;           // floats: Q buffer inside the symmetric region
   uint32_t* nvls_epoch = nullptr;  // device (workspace), kNvlsMaxCtas counters
   bool nvls_fusable = false;       // acp_step: all-reduce inside the decode prologue
+  bool tc5k1_ok = false;           // tcgen05 K1 usable: every TMA-able layer's gradient 16-B aligned
   std::vector<CUtensorMap> tmaps;  // TC path: host copy of the per-layer TMA maps
   int64_t launches = 0;
   bool plan_only = false;  // acp_plan_create: host plan, no device state
@@ -916,7 +959,10 @@ acp_status run_k1(acp_ctx* c, int parity, const Launch& ln, cudaStream_t s) {
   const int ef = c->P.ef ? 1 : 0;
   ProfRec* r = prof_begin(c, parity == 0 ? ACP_K_PROJ_P : ACP_K_PROJ_Q, ln.bytes, s);
   cudaError_t e;
-  if (ln.kind == 3) {
+  if (ln.kind == 5) {
+    e = launch_tc5_k1p(c->P.R8, c->tab, dev_tcsegs(c, ln), ln.nitems,
+                       reinterpret_cast<int32_t*>(c->ws + c->P.off_tc5sched) + 4, ln.ncta, s);
+  } else if (ln.kind == 3) {
     e = launch_tc(ln.mode, c->P.R8, c->tab, dev_tcsegs(c, ln), dev_ctab(c, ln), ln.ncta, ln.stages,
                   ln.stage_floats, 1.0f, s);
     if (e == cudaSuccess && ln.mode == 1 && ln.nred > 0) {
@@ -943,6 +989,17 @@ acp_status run_k1(acp_ctx* c, int parity, const Launch& ln, cudaStream_t s) {
   if (e != cudaSuccess) return cuda_fail(c, e, "projection kernel launch");
   ++c->launches;
   return ACP_OK;
+}
+
+// K1 over every tensor: the tcgen05 P-step when planned and usable, else k1_all
+acp_status run_k1_all(acp_ctx* c, int parity, cudaStream_t s) {
+  const Plan& P = c->P;
+  if (parity == 0 && P.tc5k1 && c->tc5k1_ok) {
+    acp_status st = run_k1(c, 0, P.k1_t5rest, s);
+    if (st != ACP_OK) return st;
+    return run_k1(c, 0, P.k1_t5, s);
+  }
+  return run_k1(c, parity, P.k1_all[parity], s);
 }
 
 acp_status run_k3(acp_ctx* c, int parity, const Launch& ln, cudaStream_t s, bool fused = false) {
@@ -1025,9 +1082,26 @@ acp_status set_grads(acp_ctx* c, float* const* grads, cudaStream_t s) {
       tc_encode_map(mp + 10, c->tab.qsplit + L.qs_off, L.m, P.R8, P.R8, true);
       tc_encode_map(mp + 11, c->tab.qsplit + L.qs_off + (int64_t)P.R8 * L.m, L.m, P.R8, P.R8, true);
       tc_encode_map(mp + 12, c->tab.qbuf + L.q_off, L.m, L.r, P.R8, true);
+      tc_encode_map(mp + 13, c->tab.qlsplit + L.qs_off, L.m, P.R8, P.R8, true);
+      tc_encode_map(mp + 14, c->tab.qlsplit + L.qs_off + (int64_t)P.R8 * L.m, L.m, P.R8, P.R8, true);
+      tc_encode_map(mp + 15, c->tab.psplit + L.ps_off, P.R8, L.n, 128, false, P.R8);
+      tc_encode_map(mp + 16, c->tab.psplit + L.ps_off + (int64_t)P.R8 * L.n, P.R8, L.n, 128, false, P.R8);
     }
     CK(c, cudaMemcpyAsync(c->ws + P.off_tmaps, c->tmaps.data(), sizeof(CUtensorMap) * c->tmaps.size(),
                           cudaMemcpyHostToDevice, s), "tensor map upload");
+    // the tcgen05 K1 streams M through TMA: usable only with 16-byte-aligned
+    // gradients; a change of that decision invalidates the captured graphs
+    bool ok = P.tc5k1;
+    for (int i = 0; ok && i < P.T; ++i)
+      if (P.L[i].mat && P.L[i].m % 4 == 0 && (reinterpret_cast<uintptr_t>(c->grads_cache[i]) & 15u) != 0) ok = false;
+    if (ok != c->tc5k1_ok) {
+      c->tc5k1_ok = ok;
+      for (auto& ge : c->gexec)
+        if (ge) {
+          cudaGraphExecDestroy(ge);
+          ge = nullptr;
+        }
+    }
   }
   return ACP_OK;
 }
@@ -1343,14 +1417,14 @@ acp_status enqueue_step(acp_ctx* c, int32_t parity, cudaStream_t s) {
   if ((st = run_orth(c, parity, s)) != ACP_OK) return st;
   const Plan& P = c->P;
   if (!P.bucketed) {
-    if ((st = run_k1(c, parity, P.k1_all[parity], s)) != ACP_OK) return st;
+    if ((st = run_k1_all(c, parity, s)) != ACP_OK) return st;
     if ((st = run_k3(c, parity, P.k3_all[parity], s)) != ACP_OK) return st;
     return ACP_OK;
   }
   if (c->nvls && c->nvls_fusable) {
     // NEXT-3: one projection launch, then the decode sums the buffer over the
     // ranks in the switch before decoding (no all-reduce launch, no comm stream)
-    if ((st = run_k1(c, parity, P.k1_all[parity], s)) != ACP_OK) return st;
+    if ((st = run_k1_all(c, parity, s)) != ACP_OK) return st;
     ProfRec* r = prof_begin(c, ACP_K_ALLREDUCE, 0.0, s);  // marker only: fused into the decode
     prof_end(r, s);
     return run_k3(c, parity, P.k3_fused[parity], s, true);
@@ -1601,7 +1675,7 @@ acp_status acp_compress(acp_ctx* c, int32_t parity, float* const* grads, float**
   if ((st = before_k1(c, parity, s)) != ACP_OK) return st;
   // Power-SGD's first projection uses the previous Q as it is
   if (!(c->P.psgd && parity == 0) && (st = run_orth(c, parity, s)) != ACP_OK) return st;
-  if ((st = run_k1(c, parity, c->P.k1_all[parity], s)) != ACP_OK) return st;
+  if ((st = run_k1_all(c, parity, s)) != ACP_OK) return st;
   after_k1(c, parity);
   *out_buffer = parity == 0 ? c->tab.pbuf : c->tab.qbuf;
   *out_count = c->P.arena[parity];

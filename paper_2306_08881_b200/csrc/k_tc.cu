@@ -1002,16 +1002,22 @@ static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
   return fn;
 }
 
-bool tc_encode_map(CUtensorMap* out, const float* base, int64_t cols, int64_t rows, int box_rows, bool atom32) {
+bool tc_encode_map(CUtensorMap* out, const float* base, int64_t cols, int64_t rows, int box_rows, bool atom32,
+                   int box_cols) {
   std::memset(out, 0, sizeof(CUtensorMap));
   auto enc = tmap_encoder();
   if (!enc || !base || cols % 4 != 0 || (reinterpret_cast<uintptr_t>(base) & 15u) != 0) return false;
   const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   const cuuint64_t strides[1] = {(cuuint64_t)cols * 4};
-  const cuuint32_t box[2] = {(cuuint32_t)kPBC, (cuuint32_t)box_rows};
+  const cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  // swizzle span = the box row: 128 B (32 floats), or 64 / 32 B for narrow boxes
+  const CUtensorMapSwizzle sw = atom32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B
+                                       : (box_cols == 8 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                                        : (box_cols == 16 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                                          : CU_TENSOR_MAP_SWIZZLE_128B));
   const cuuint32_t estr[2] = {1, 1};
   return enc(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, atom32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }

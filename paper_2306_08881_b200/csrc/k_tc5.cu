@@ -43,6 +43,7 @@
 
 #include "k_common.cuh"
 #include "k_nvls.cuh"
+#include "k_umma.cuh"
 
 namespace acp {
 namespace {
@@ -80,45 +81,10 @@ __device__ __forceinline__ uint32_t atom_off(int mn, int k) {
                     ((((mn & 31) >> 3) ^ (k & 3)) << 5) + (mn & 7) * 4);
 }
 
-// UMMA shared-memory descriptor: SWIZZLE_128B_BASE32B (layout type 1),
-// MN-major (LBO = stride of the 32-element MN blocks, SBO = stride of the
-// 4-deep K groups), Blackwell descriptor version 1
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
-         ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46) | (1ull << 61);
+  return umma_sdesc(saddr, lbo, sbo, kLayoutSw128Atom32);
 }
-// instruction descriptor: D fp32, A / B tf32, both MN-major, M x N
-__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | (1u << 16) | ((uint32_t)(N >> 3) << 17) |
-         ((uint32_t)(M >> 4) << 24);
-}
-
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void umma_tf32(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
-      "l"(a), "l"(b), "r"(idesc), "r"(acc)
-      : "memory");
-}
-// arrive on `bar` when every tcgen05 operation this thread issued so far is done
-__device__ __forceinline__ void umma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(s32(bar))
-               : "memory");
-}
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
-        "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
-        "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
-        "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) { return umma_idesc_tf32(M, N, 1, 1); }
 
 // grad[i] = scale * slot[i], i in [i0, i1), by one warp: 8 loads in flight
 // per lane (the slot is 16-byte aligned; float4 when the gradient is too)
@@ -193,11 +159,7 @@ struct T5Bars {
 };
 
 // Consumer view of the item ring: item number c (0, 1, ...) of this CTA.
-__device__ __forceinline__ int ring_read(const T5Bars& b, uint32_t c) {
-  const int slot = c % kT5Ring;
-  mbar_wait(&b.sfull[slot], (c / kT5Ring) & 1u);
-  return *reinterpret_cast<volatile int32_t*>(b.ring + slot);
-}
+__device__ __forceinline__ int ring_read(const T5Bars& b, uint32_t c) { return acp::ring_read(b.sfull, b.ring, kT5Ring, c); }
 
 template <int MODE, int R8>
 __global__ void __launch_bounds__(kT5Threads, 1)
@@ -247,10 +209,7 @@ tc5_decode_kernel(Tables t, const TcSeg* __restrict__ items, int nitems, int32_t
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(s32(b.tmem)),
-                 "r"(kT5TmemCols)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    tmem_alloc(b.tmem, kT5TmemCols);
   }
   tc_fence_before();
   __syncthreads();
@@ -380,7 +339,10 @@ tc5_decode_kernel(Tables t, const TcSeg* __restrict__ items, int nitems, int32_t
           mbar_wait(&b.tfull[acc], (t_it / kT5Acc) & 1u);
           tc_fence_after();
           uint32_t v[32];
-          if (na > 0) tmem_ld32(tbase + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * kT5M + 32 * jc), v);
+          if (na > 0) {
+            tmem_ld_x32(tbase + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * kT5M + 32 * jc), v);
+            tmem_wait_ld();
+          }
           // this warp's part of the accumulator is drained: the MMA may refill
           // it once every epilogue warp has arrived
           tc_fence_before();
@@ -519,18 +481,9 @@ tc5_decode_kernel(Tables t, const TcSeg* __restrict__ items, int nitems, int32_t
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(kT5TmemCols)
-                 : "memory");
+    tmem_dealloc(tbase, kT5TmemCols);
   }
-  // the last CTA out re-arms the item counter for the next launch (graph-safe)
-  if (threadIdx.x == 0) {
-    __threadfence();
-    if (atomicAdd(sched + 1, 1) == (int)gridDim.x - 1) {
-      sched[0] = 0;
-      sched[1] = 0;
-      __threadfence();
-    }
-  }
+  sched_rearm(sched);
 }
 
 }  // namespace
