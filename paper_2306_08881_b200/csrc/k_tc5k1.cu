@@ -43,10 +43,11 @@ struct K1 {
   static constexpr int TILE = kK1M * kK1N * 4;        // 16 KB: 128 rows x 32 columns
   static constexpr int FBOX = R8 * kK1N * 4;          // factor box: R8 rows x 32 columns
   static constexpr int STAGE = 3 * TILE + 4 * FBOX;   // M (-> x_hi), S (-> x), x_lo, Qo hi/lo, Ql hi/lo
-  static constexpr int NS = R8 >= 32 ? 2 : 3;
+  static constexpr int NS = R8 >= 16 ? 3 : 4;
   static constexpr int PO = kK1M * R8 * 4;            // P_orth rows of a block (hi or lo)
-  static constexpr int PO_OFF = NS * STAGE;           // [2 buffers][hi, lo]
-  static constexpr int BAR_OFF = PO_OFF + 4 * PO;
+  static constexpr int NPO = R8 >= 32 ? 1 : 2;        // P_orth buffers
+  static constexpr int PO_OFF = NS * STAGE;           // [NPO buffers][hi, lo]
+  static constexpr int BAR_OFF = PO_OFF + NPO * 2 * PO;
   static constexpr int SMEM = BAR_OFF + 512 + 1024;
   static constexpr uint32_t PO_LAYOUT = R8 == 8 ? kLayoutSw32 : (R8 == 16 ? kLayoutSw64 : kLayoutSw128);
   // MMA 2 width: N >= 16 for M = 128 (at R8 = 8 the extra 8 columns read the
@@ -156,8 +157,8 @@ tc5_k1p_kernel(Tables t, const TcSeg* __restrict__ items, int nitems, int32_t* _
           tmap_acquire(maps + 14);
           tmap_acquire(maps + 15);
           tmap_acquire(maps + 16);
-          const int pb = b_it & 1;
-          mbar_wait(&b.poempty[pb], ((b_it >> 1) & 1u) ^ 1u);
+          const int pb = b_it % G::NPO;
+          mbar_wait(&b.poempty[pb], ((b_it / G::NPO) & 1u) ^ 1u);
           unsigned char* po = base + G::PO_OFF + pb * 2 * G::PO;
           mbar_arrive_tx(&b.pofull[pb], 2u * G::PO);
           tma_load_2d(po, maps + 15, 0, (int)s.row0, &b.pofull[pb], pol_keep);
@@ -195,8 +196,8 @@ tc5_k1p_kernel(Tables t, const TcSeg* __restrict__ items, int nitems, int32_t* _
         const LayerDesc& L = t.layers[s.layer];
         if (L.mat) {
           const uint32_t ntiles = (uint32_t)((L.m + kK1N - 1) / kK1N);
-          const int pb = b_it & 1;
-          mbar_wait(&b.pofull[pb], (b_it >> 1) & 1u);
+          const int pb = b_it % G::NPO;
+          mbar_wait(&b.pofull[pb], (b_it / G::NPO) & 1u);
           const uint32_t poh = sbase + G::PO_OFF + pb * 2 * G::PO, pol = poh + G::PO;
           auto corr = [&](uint32_t tt) {
             const int st = tt % NS, ca = tt & 1;
@@ -336,6 +337,7 @@ tc5_k1p_kernel(Tables t, const TcSeg* __restrict__ items, int nitems, int32_t* _
   } else {
     // ---------------- storer: S tiles back to global (TMA) + 1-D tensors ----------------
     uint32_t t_it = 0;
+    int pend = -1;  // stage whose store is issued but not yet released
     for (uint32_t c = 0;; ++c) {
       const int cur = ring_read(b.sfull, b.ring, kK1Ring, c);
       if (cur < 0) break;
@@ -353,6 +355,8 @@ tc5_k1p_kernel(Tables t, const TcSeg* __restrict__ items, int nitems, int32_t* _
             if (e + 32 * u < s.row1) slot[e + 32 * u] = v[u];
         }
       } else if (lane == 0) {
+        // one bulk group per tile; a stage's S tile is released once its
+        // store has been READ (one group behind, so stores overlap)
         const CUtensorMap* smap = t.tmaps + kTmapsPerLayer * (int64_t)s.layer + 1;
         tmap_acquire(smap);
         for (int64_t c0 = 0; c0 < L.m; c0 += kK1N, ++t_it) {
@@ -360,15 +364,21 @@ tc5_k1p_kernel(Tables t, const TcSeg* __restrict__ items, int nitems, int32_t* _
           mbar_wait(&b.xready[st], (t_it / NS) & 1u);
           tma_store_2d(smap, stage_ptr(t_it) + G::S_S, (int)c0, (int)s.row0);
           bulk_commit();
-          bulk_wait_read<0>();
-          mbar_arrive(&b.sfree[st]);
+          if (pend >= 0) {
+            bulk_wait_read<1>();
+            mbar_arrive(&b.sfree[pend]);
+          }
+          pend = st;
         }
       }
       if (L.mat) t_it = __shfl_sync(0xffffffffu, t_it, 0);
       __syncwarp();
       if (lane == 0) mbar_arrive(&b.sempty[c % kK1Ring]);
     }
-    if (lane == 0) bulk_wait_all();
+    if (lane == 0) {
+      bulk_wait_all();
+      if (pend >= 0) mbar_arrive(&b.sfree[pend]);
+    }
   }
   tc_fence_before();
   __syncthreads();
