@@ -174,6 +174,8 @@ struct Tables {
   const NvlsArgs* nv;
   FusedSync* fsync;
   int32_t* nonfinite;  // sticky flag: bit 0 K2 saw a non-finite factor, bit 1 finite scan hit
+  int32_t stream_pf;   // stream kernels: tiles prefetched into L2 ahead of the shared ring (0: off)
+  int32_t tc5_pf;      // tcgen05 K1: M / S tiles prefetched into L2 ahead
   int32_t nvls_fused;
 };
 // TC path TMA maps per layer: [M, S, Q_orth hi, lo, Q_loc hi, lo] (P-step

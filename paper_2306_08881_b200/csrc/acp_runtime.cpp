@@ -1199,6 +1199,10 @@ acp_status acp_create(const acp_config* cfg, acp_ctx** out) {
   t.fsync = reinterpret_cast<FusedSync*>(c->ws + P.off_fsync);
   t.nvls_fused = 0;
   t.nonfinite = reinterpret_cast<int32_t*>(c->ws + P.off_nonfinite);
+  t.stream_pf = std::getenv("ACP_STREAM_PF") ? std::atoi(std::getenv("ACP_STREAM_PF")) : 0;
+  // L2 prefetch ahead of the shared-memory rings: measured slower everywhere
+  // (BERT-L r=4 / r=8 / r=32, ResNet-50), off by default; A/B switches
+  t.tc5_pf = std::getenv("ACP_TC5_PF") ? std::atoi(std::getenv("ACP_TC5_PF")) : 0;
   c->nvls_epoch = reinterpret_cast<uint32_t*>(c->ws + P.off_nvepoch);
 
   DeviceGuard dg(cfg->device);

@@ -168,6 +168,17 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(r0), "r"(s32(bar)), "l"(policy)
       : "memory");
 }
+// L2 prefetch of a tensor-map box (no shared memory, no completion): keeps
+// more HBM reads in flight than the shared-memory ring can hold
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int r0) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(r0)
+               : "memory");
+}
+// L2 prefetch of `bytes` (multiple of 16) at a 16-byte-aligned address
+__device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void tmap_acquire(const CUtensorMap* map) {
   asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(
                    reinterpret_cast<uint64_t>(map))

@@ -129,8 +129,21 @@ __device__ void producer(const Tables& t, const StreamSeg* segs, int sb, int se,
     const float* pe = t.E + L.e_off + s.row0 * m + c0;
     const float* Pf = t.pbuf + L.p_off;
     const int RTp = sh.ptile > 0 ? sh.ptile / tr : 0;  // row stride in sP (>= r)
+    // L2 prefetch of the tiles t.stream_pf ahead of the ring (whole-row
+    // tiles): more HBM reads in flight than the shared-memory stages hold
+    const int pf = (cols == m) ? t.stream_pf : 0;
+    auto prefetch_tile = [&](int64_t rp) {
+      if (rp < s.row1) {
+        const uint32_t pb = (uint32_t)(((s.row1 - rp) < tr ? (s.row1 - rp) : tr) * m * 4);
+        bulk_prefetch_l2(grad + rp * m, pb);
+        bulk_prefetch_l2(t.E + L.e_off + rp * m, pb);
+      }
+    };
+    if (pf > 0 && lane == 0)
+      for (int j = 1; j <= pf; ++j) prefetch_tile(s.row0 + (int64_t)j * tr);
     for (int64_t r0 = s.row0; r0 < s.row1; r0 += tr) {
       const int64_t nr = (s.row1 - r0) < tr ? (s.row1 - r0) : tr;
+      if (pf > 0 && lane == 0 && r0 > s.row0) prefetch_tile(r0 + (int64_t)pf * tr);
       if (lane == 0) mbar_wait(&sh.empty[stage], phase ^ 1u);
       __syncwarp();
       if (lane == 0) {

@@ -20,8 +20,9 @@
 //     long, 12 MMAs) and write P_loc at the end of the block.
 // 12 B / element of HBM (read M, S; write S), like the mma.sync kernel; the
 // rank-r products are tensor-core work. CTA roles: warp 0 fetcher + TMA
-// producer, warp 1 TMEM owner + MMA issuer, warps 2-5 converters (TMEM lane
-// quarter = warp % 4), warp 6 S-tile TMA storer + 1-D tensors (pack).
+// producer, warp 1 TMEM owner + MMA issuer, warps 2-9 converters (two per
+// TMEM lane quarter = warp % 4, 16 columns each), warp 10 S-tile TMA storer +
+// 1-D tensors (pack).
 #include <cuda.h>
 
 #include "k_common.cuh"
@@ -32,9 +33,11 @@ namespace {
 
 constexpr int kK1M = 128;         // rows per block (MMA M, TMEM lanes)
 constexpr int kK1N = 32;          // columns per tile (one 128-byte box)
-constexpr int kK1Threads = 224;   // 7 warps
+constexpr int kK1Conv = 8;        // converter warps: 2 per TMEM lane quarter, 16 columns each
+constexpr int kK1Threads = 32 * (3 + kK1Conv);  // + producer, MMA, storer
+constexpr int kK1WarpStore = 2 + kK1Conv;
 constexpr int kK1Ring = 8;        // item slots
-constexpr int kK1SlotReaders = 1 + 4 + 1;  // MMA thread, converter warps, storer warp
+constexpr int kK1SlotReaders = 1 + kK1Conv + 1;  // MMA thread, converter warps, storer warp
 constexpr int kK1TmemCols = 128;  // corr 2 x 32 at [0, 64); P partials 2 x PN at [64, 64 + 2 PN)
 
 template <int R8>
@@ -60,10 +63,10 @@ struct K1 {
 
 struct K1Bars {
   uint64_t *sfull, *sempty;    // [kK1Ring] item ring
-  uint64_t *full, *xready;     // [NS] TMA landed / converters wrote x (4 arrivals)
+  uint64_t *full, *xready;     // [NS] TMA landed / converters wrote x (kK1Conv arrivals)
   uint64_t *pdone, *sfree;     // [NS] MMA 2 read the stage / storer's TMA store read S
-  uint64_t *cfull, *cempty;    // [2] corr accumulator (MMA commit / 4 arrivals)
-  uint64_t *qfull, *qempty;    // [2] P partial (MMA commit / 4 arrivals)
+  uint64_t *cfull, *cempty;    // [2] corr accumulator (MMA commit / kK1Conv arrivals)
+  uint64_t *qfull, *qempty;    // [2] P partial (MMA commit / 4 arrivals: the h = 0 converters)
   uint64_t *pofull, *poempty;  // [2] P_orth rows (TMA / MMA commit)
   int32_t* ring;
   uint32_t* tmem;
@@ -103,13 +106,13 @@ tc5_k1p_kernel(Tables t, const TcSeg* __restrict__ items, int nitems, int32_t* _
     }
     for (int i = 0; i < NS; ++i) {
       mbar_init(&b.full[i], 1);
-      mbar_init(&b.xready[i], 4);
+      mbar_init(&b.xready[i], kK1Conv);
       mbar_init(&b.pdone[i], 1);
       mbar_init(&b.sfree[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&b.cfull[i], 1);
-      mbar_init(&b.cempty[i], 4);
+      mbar_init(&b.cempty[i], kK1Conv);
       mbar_init(&b.qfull[i], 1);
       mbar_init(&b.qempty[i], 4);
       mbar_init(&b.pofull[i], 1);
@@ -142,6 +145,7 @@ tc5_k1p_kernel(Tables t, const TcSeg* __restrict__ items, int nitems, int32_t* _
       uint64_t pol_keep;
       asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
       uint32_t t_it = 0, b_it = 0;
+      bool c_first = true;
       int cur = fetch();
       int nxt = cur >= 0 ? fetch() : -1;
       while (cur >= 0) {
@@ -164,7 +168,33 @@ tc5_k1p_kernel(Tables t, const TcSeg* __restrict__ items, int nitems, int32_t* _
           tma_load_2d(po, maps + 15, 0, (int)s.row0, &b.pofull[pb], pol_keep);
           tma_load_2d(po + G::PO, maps + 16, 0, (int)s.row0, &b.pofull[pb], pol_keep);
           ++b_it;
+          // L2 prefetch of the M / S tiles t.tc5_pf tiles ahead (this block's
+          // later tiles, then the next item's first ones)
+          const int64_t ntile = (L.m + kK1N - 1) / kK1N;
+          const TcSeg sn = items[nxt >= 0 ? nxt : cur];
+          const LayerDesc& Ln = t.layers[sn.layer];
+          const CUtensorMap* mapsn = t.tmaps + kTmapsPerLayer * (int64_t)sn.layer;
+          const bool pf_next = nxt >= 0 && Ln.mat;
+          if (pf_next) {
+            tmap_acquire(mapsn + 0);
+            tmap_acquire(mapsn + 1);
+          }
+          auto prefetch = [&](int64_t j) {  // tile j of this block (j >= ntile: of the next one)
+            if (j < ntile) {
+              tma_prefetch_2d(maps + 0, (int)(j * kK1N), (int)s.row0);
+              tma_prefetch_2d(maps + 1, (int)(j * kK1N), (int)s.row0);
+            } else if (pf_next && (j - ntile) * kK1N < Ln.m) {
+              tma_prefetch_2d(mapsn + 0, (int)((j - ntile) * kK1N), (int)sn.row0);
+              tma_prefetch_2d(mapsn + 1, (int)((j - ntile) * kK1N), (int)sn.row0);
+            }
+          };
+          const int kPF = t.tc5_pf;
+          if (c_first) {  // the CTA's first block: warm the first kPF tiles too
+            for (int64_t j = 0; j < kPF; ++j) prefetch(j);
+            c_first = false;
+          }
           for (int64_t c0 = 0; c0 < L.m; c0 += kK1N, ++t_it) {
+            if (kPF > 0) prefetch(c0 / kK1N + kPF);
             const int st = t_it % NS;
             const uint32_t ph = (t_it / NS) & 1u;
             mbar_wait(&b.pdone[st], ph ^ 1u);
@@ -248,9 +278,12 @@ tc5_k1p_kernel(Tables t, const TcSeg* __restrict__ items, int nitems, int32_t* _
         mbar_arrive(&b.sempty[c % kK1Ring]);
       }
     }
-  } else if (warp < 6) {
+  } else if (warp < kK1WarpStore) {
     // ---------------- converters: x = M + S - corr; P_loc accumulation ----------------
+    // two warps per TMEM lane quarter split the tile's 32 columns; the h = 0
+    // warp of a quarter also accumulates its rows' P_loc
     const int q = warp & 3;
+    const int h = (warp - 2) >> 2;
     const int i = 32 * q + lane;  // row within the block (= TMEM lane)
     uint32_t t_it = 0;
     for (uint32_t c = 0;; ++c) {
@@ -283,23 +316,24 @@ tc5_k1p_kernel(Tables t, const TcSeg* __restrict__ items, int nitems, int32_t* _
           mbar_wait(&b.full[st], (tt / NS) & 1u);
           mbar_wait(&b.cfull[ca], (tt >> 1) & 1u);
           tc_fence_after();
-          uint32_t cv[32];
-          tmem_ld_x32(tbase + ((uint32_t)(32 * q) << 16) + (uint32_t)(ca * kK1N), cv);
+          uint32_t cv[16];
+          tmem_ld_x16(tbase + ((uint32_t)(32 * q) << 16) + (uint32_t)(ca * kK1N + 16 * h), cv);
           tmem_wait_ld();
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&b.cempty[ca]);
           unsigned char* sp = stage_ptr(tt);
 #pragma unroll
-          for (int ch = 0; ch < 8; ++ch) {
+          for (int cc = 0; cc < 4; ++cc) {
+            const int ch = 4 * h + cc;
             const int off = i * 128 + ((ch ^ sw) << 4);
             const float4 mv = *reinterpret_cast<const float4*>(sp + G::S_M + off);
             const float4 sv = *reinterpret_cast<const float4*>(sp + G::S_S + off);
             float4 x;
-            x.x = mv.x + sv.x - __uint_as_float(cv[4 * ch + 0]);
-            x.y = mv.y + sv.y - __uint_as_float(cv[4 * ch + 1]);
-            x.z = mv.z + sv.z - __uint_as_float(cv[4 * ch + 2]);
-            x.w = mv.w + sv.w - __uint_as_float(cv[4 * ch + 3]);
+            x.x = mv.x + sv.x - __uint_as_float(cv[4 * cc + 0]);
+            x.y = mv.y + sv.y - __uint_as_float(cv[4 * cc + 1]);
+            x.z = mv.z + sv.z - __uint_as_float(cv[4 * cc + 2]);
+            x.w = mv.w + sv.w - __uint_as_float(cv[4 * cc + 3]);
             *reinterpret_cast<float4*>(sp + G::S_S + off) = x;
             uint4 h, l;
             split_tf32(x.x, h.x, l.x);
@@ -312,11 +346,11 @@ tc5_k1p_kernel(Tables t, const TcSeg* __restrict__ items, int nitems, int32_t* _
           fence_async_smem();
           __syncwarp();
           if (lane == 0) mbar_arrive(&b.xready[st]);
-          if (j > 0) add_partial(tt - 1);
+          if (h == 0 && j > 0) add_partial(tt - 1);
         }
-        add_partial(t_it + ntiles - 1);
+        if (h == 0) add_partial(t_it + ntiles - 1);
         const int64_t row = s.row0 + i;
-        if (row < s.row1) {
+        if (h == 0 && row < s.row1) {
           const int64_t n = L.n;
           float* Pw = t.pbuf + L.p_off;       // P slot, k-major [r][n]
           float* Pl = t.plsplit + L.ps_off;   // P_loc split [2][n][R8]
