@@ -85,6 +85,9 @@ struct Plan {
   // such layer's gradient is 16-byte aligned (acp_ctx::tc5k1_ok), else k1_all
   bool tc5k1 = false;
   Launch k1_t5, k1_t5rest;
+  // SIMT K1-P' split by layer width (ACP_K1P_SPLIT): the wide layers' staged
+  // local factor no longer sets the ring depth of the narrow ones
+  Launch k1_wide;
   Launch k3_fused[2];  // decodes planned as one resident wave (NVLS-fused prologue)
   // world_size > 1: compute groups = runs of consecutive buckets whose
   // projection / decode run as one launch; each bucket is still its own
@@ -211,7 +214,11 @@ acp_status build_plan(const acp_config* cfg, Plan& P, bool plan_only = false) {
          (P.RT >= 8 || (tc_env && std::atoi(tc_env) != 0));
   P.R8 = P.tc ? std::max(8, (P.RT + 7) / 8 * 8) : 0;
   P.tc5 = P.tc && !std::getenv("ACP_NO_TC5");
-  P.tc5k1 = P.tc5 && !std::getenv("ACP_NO_TC5K1");
+  // tcgen05 K1 P-step: faster than the mma.sync kernel at r = 32 (BERT-L
+  // proj_p 1.22 -> 1.09 ms), slower at r = 16 (0.93 -> 0.99) and r = 8
+  // (BERT-Base 0.28 -> 0.31): default at R8 = 32; ACP_TC5K1=1 / 0 forces it
+  const char* k1env = std::getenv("ACP_TC5K1");
+  P.tc5k1 = P.tc5 && !std::getenv("ACP_NO_TC5K1") && (k1env ? std::atoi(k1env) != 0 : P.R8 >= 32);
   int tc_q_stage = 0;
   // offsets
   int64_t e = 0, ql = 0, w = 0, so[2] = {0, 0}, qs = 0, ps = 0;
@@ -261,7 +268,16 @@ acp_status build_plan(const acp_config* cfg, Plan& P, bool plan_only = false) {
       L.pw = kThreads * L.W;
       // TMA stream kernels: thread mapping per mode (tr == 0: generic path)
       if (P.ef) {
-        stream_make_map(0, L.m, P.RT, &L.sm[0]);
+        // A/B knobs (measured, off by default): half-size K1-P' tiles for the
+        // wide layers (ACP_K1P_WIDE_TT), splitting K1-P' by width
+        // (ACP_K1P_SPLIT) and a larger ring budget (ACP_STREAM_BUDGET_KB)
+        // give the narrow layers 3 ring stages, but the step is not faster
+        // (BERT-L r=4 1.031-1.044 vs 1.027 ms): K1-P' is issue/latency-bound,
+        // not ring-depth-bound (scripts/micro/read_pattern.cu streams this
+        // traffic at 100% of the copy peak with 3 x 64 KB stages)
+        static const int wide_m = std::getenv("ACP_K1P_WIDE") ? std::atoi(std::getenv("ACP_K1P_WIDE")) : 4096;
+        static const int wide_tt = std::getenv("ACP_K1P_WIDE_TT") ? std::atoi(std::getenv("ACP_K1P_WIDE_TT")) : 0;
+        stream_make_map(0, L.m, P.RT, &L.sm[0], (wide_m > 0 && L.m >= wide_m && P.RT <= 4) ? wide_tt : 0);
         // K1-P stages the layer's local Q (RT x m) next to two ring stages
         const StreamMap& m0 = L.sm[0];
         if (m0.tr > 0 && 4 * ((int64_t)P.RT * L.m + 4LL * m0.tr * m0.pcols + 2LL * m0.tr * P.RT) +
@@ -477,7 +493,8 @@ acp_status build_plan(const acp_config* cfg, Plan& P, bool plan_only = false) {
     // row stride RT in sP; the kernel derives it as ptile / tr per layer, so
     // size per-layer slots as tr_layer * RT and reserve max_tr * RT per stage
     ln.ptile = need_p ? (int)(max_tr * P.RT) : 0;
-    const int64_t budget = (cps == 1 ? 200 : 96) * 1024 - 4 * factor_floats;
+    static const int budget_kb = std::getenv("ACP_STREAM_BUDGET_KB") ? std::atoi(std::getenv("ACP_STREAM_BUDGET_KB")) : 200;
+    const int64_t budget = (cps == 1 ? budget_kb : 96) * 1024 - 4 * factor_floats;
     int stages = (int)std::min<int64_t>(8, budget / (2 * 4 * stage_floats + 4 * ln.ptile));
     ln.stages = std::max(2, stages);
     ln.stage_floats = (int)stage_floats;
@@ -673,6 +690,16 @@ acp_status build_plan(const acp_config* cfg, Plan& P, bool plan_only = false) {
   for (int i = 0; i < P.T; ++i) all[i] = i;
   for (int p = 0; p < 2; ++p) {
     P.k1_all[p] = k1_launch(p, all);
+    static const bool split = std::getenv("ACP_K1P_SPLIT") ? std::atoi(std::getenv("ACP_K1P_SPLIT")) != 0 : false;
+    if (p == 0 && split && use_stream && P.defer) {
+      static const int wide_m = std::getenv("ACP_K1P_WIDE") ? std::atoi(std::getenv("ACP_K1P_WIDE")) : 4096;
+      std::vector<int> narrow, wide;
+      for (int i : all) (P.L[i].mat && P.L[i].m >= wide_m ? wide : narrow).push_back(i);
+      if (!wide.empty() && !narrow.empty()) {
+        P.k1_all[0] = k1_launch(0, narrow);
+        P.k1_wide = k1_launch(0, wide);
+      }
+    }
     if (p == 0 && P.tc5k1) {
       // tcgen05 P-step: 128-row blocks of every matrix with m % 4 == 0
       // (largest rows first), then vector chunks; the rest via mma.sync
@@ -999,7 +1026,9 @@ acp_status run_k1_all(acp_ctx* c, int parity, cudaStream_t s) {
     if (st != ACP_OK) return st;
     return run_k1(c, 0, P.k1_t5, s);
   }
-  return run_k1(c, parity, P.k1_all[parity], s);
+  acp_status st = run_k1(c, parity, P.k1_all[parity], s);
+  if (st == ACP_OK && parity == 0 && P.k1_wide.ncta > 0) st = run_k1(c, 0, P.k1_wide, s);
+  return st;
 }
 
 acp_status run_k3(acp_ctx* c, int parity, const Launch& ln, cudaStream_t s, bool fused = false) {

@@ -917,13 +917,14 @@ int stream_ctas_per_sm(int mode) {
   return mode == 0 ? Cfg<0>::CPS : (mode == 2 ? Cfg<2>::CPS : Cfg<3>::CPS);
 }
 
-bool stream_make_map(int mode, int64_t m, int rt, StreamMap* out) {
+bool stream_make_map(int mode, int64_t m, int rt, StreamMap* out, int tt_override) {
   *out = StreamMap{};
   if (m % 4 != 0 || rt > 8) return false;
   const int NW = nw_of(mode, rt);
   // K1-P at r = 8 stages an 8 x m local factor: halve its tiles to stay in 227 KB
-  const int64_t TT = mode == 0 ? (rt >= 8 ? Cfg<0>::TT / 2 : Cfg<0>::TT)
-                               : (mode == 2 ? Cfg<2>::TT : Cfg<3>::TT);
+  int64_t TT = mode == 0 ? (rt >= 8 ? Cfg<0>::TT / 2 : Cfg<0>::TT)
+                         : (mode == 2 ? Cfg<2>::TT : Cfg<3>::TT);
+  if (tt_override > 0) TT = tt_override;
   const int ncm = nc_max(mode, rt);
   if (ncm <= 0) return false;
   const int64_t m4 = m / 4;

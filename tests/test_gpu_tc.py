@@ -67,3 +67,46 @@ def test_tc_graph_replay_and_determinism():
     for a, b in zip(outs[0], outs[2]):
         for x, y in zip(a, b):
             assert torch.equal(x, y)
+
+
+# -- kernel selection on the tensor-core path: the tcgen05 decodes (k_tc5.cu,
+# default for r >= 8) and tcgen05 K1 P-step (k_tc5k1.cu, default at r = 32)
+# forced on / off at every tensor-core rank, so each kernel variant meets the
+# oracle on the ragged set (m % 4 != 0 layers, rank clamps, vectors).
+@pytest.mark.parametrize("env", [{"ACP_TC5K1": "1"}, {"ACP_TC5K1": "0"}, {"ACP_NO_TC5": "1"}])
+@pytest.mark.parametrize("rank", [8, 16, 32])
+def test_tc_kernel_variants(monkeypatch, env, rank):
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    inputs = make_inputs(RAGGED, 2, 5, SEED, "lowrank")
+    q0 = make_q0(RAGGED, rank, SEED)
+    gpu = run_gpu_simulated(RAGGED, rank, inputs, q0=q0, seed=SEED)
+    ref = run_oracle(RAGGED, rank, inputs, q0=q0, seed=SEED)
+    compare(RAGGED, gpu, ref, inputs)
+
+
+def test_tc5k1_unaligned_gradients_fall_back():
+    """The tcgen05 K1 streams M through TMA and needs 16-byte-aligned
+    gradients; misaligned views switch the step to the mma.sync kernel (and
+    re-capture the graph) with identical results to the oracle."""
+    import torch
+    from paper_2306_08881_b200 import AcpContext
+    from oracle import AcpOracle, rel_frobenius
+    shapes = [(300, 1024), (64,), (130, 256)]
+    q0 = make_q0(shapes, 32, SEED)
+    ctx = AcpContext(shapes, 32, seed=SEED, q0=q0)
+    o = AcpOracle(shapes, 32, seed=SEED, q0=q0)
+    for t in range(6):
+        g = [np.random.default_rng([t, i]).standard_normal(s).astype(np.float32) for i, s in enumerate(shapes)]
+        views = []
+        for x in g:
+            off = 1 if t in (2, 3) else 0      # steps 2-3: 4-byte offset, not 16-byte aligned
+            base = torch.empty(x.size + off, device="cuda")
+            v = base[off:].view(x.shape)
+            v.copy_(torch.from_numpy(x))
+            views.append(v)
+        ctx.step(views, t % 2)
+        ref = o.step([g], t % 2)
+        for a, b in zip(views, ref):
+            assert rel_frobenius(a.cpu().numpy(), b) < 1e-4
+    ctx.close()
