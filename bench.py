@@ -413,15 +413,25 @@ def _roofline(prof, peak, peak_kind, workload):
     per_launch_bytes = d["bytes"] / d["launches"]
     per_launch_ms = d["ms"] / d["launches"]
     achieved = per_launch_bytes / (per_launch_ms * 1e-3) / 1e9
-    traffic = None
+    # DRAM traffic of the dominant kernel from an ncu capture of THIS build
+    # (profiles/ncu_traffic_<tag>.json, build id = source hash, build.py)
+    traffic, tsrc = None, None
     try:
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            tr = json.load(f)
-        traffic = tr.get(workload, {}).get(dom)
+        import glob
+        import importlib.util
+        spec = importlib.util.spec_from_file_location("acp_build", os.path.join(ROOT, "paper_2306_08881_b200", "build.py"))
+        B = importlib.util.module_from_spec(spec)
+        spec.loader.exec_module(B)
+        bid = B.build_id()
+        for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "ncu_traffic_*.json")), reverse=True):
+            tr = json.load(open(f))
+            if tr.get("build_id") == bid and dom in tr.get(workload, {}):
+                traffic, tsrc = tr[workload][dom], os.path.relpath(f, ROOT) + f" (build {bid})"
+                break
     except Exception:
         pass
     return {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
+            "frac": achieved / peak, "traffic": traffic, "traffic_source": tsrc, "peak_source": peak_kind,
             "algorithmic_bytes_per_launch": per_launch_bytes, "ms_per_launch": per_launch_ms,
             "per_class": {k: {"ms_per_launch": v["ms"] / v["launches"],
                               "gbs": (v["bytes"] / v["launches"]) / (v["ms"] / v["launches"] * 1e-3) / 1e9}

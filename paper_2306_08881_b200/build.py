@@ -45,6 +45,20 @@ def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp")))
 
 
+def build_id() -> str:
+    """Content hash of the library sources (csrc/ + include/acp.h): ties
+    measurement artefacts (profiles/ncu_traffic_*.json) to the build they
+    were captured on."""
+    import hashlib
+    h = hashlib.sha256()
+    for f in sorted(glob.glob(os.path.join(CSRC, "*"))) + [os.path.join(ROOT, "include", "acp.h")]:
+        if os.path.isfile(f):
+            h.update(os.path.basename(f).encode())
+            with open(f, "rb") as fh:
+                h.update(fh.read())
+    return h.hexdigest()[:16]
+
+
 def _stale(target, deps):
     if not os.path.exists(target):
         return True
@@ -87,6 +101,8 @@ def build(verbose: bool = False, force: bool = False) -> str:
         if p.returncode != 0:
             sys.stderr.write(" ".join(link) + "\n" + p.stdout + p.stderr)
             raise RuntimeError("link failed")
+    with open(os.path.join(OUT_DIR, "build_id.txt"), "w") as f:
+        f.write(build_id() + "\n")
     return LIB_PATH
 
 
