@@ -101,6 +101,8 @@ __device__ __noinline__ void chol_inv_regs(const Tables& t, const LayerDesc& L, 
     for (int i = 0; i < RT; ++i)
       if (i < r) Wout[i * r + l] = (i <= l) ? w[i] : 0.0;
   }
+  __threadfence();  // every lane's W columns visible before lane 0 publishes (see orth_item)
+  __syncwarp();
   const uint32_t dmask = __ballot_sync(0xffffffffu, mydg && l < r);
   const bool anynf = __any_sync(0xffffffffu, nonfinite);
   if (l == 0) {
@@ -350,6 +352,13 @@ __device__ void orth_item(const Tables& t, int side, const OrthSeg& s, int phase
         Wout[i * r + l] = w;
       }
     }
+    // every lane's W columns must be visible GPU-wide before lane 0 publishes
+    // the flag the next phase's items (other SMs) wait on: without this, lane
+    // 0 could publish while lanes 1..r-1 had not stored (or made visible)
+    // their columns, and a phase-1/2 item read a stale column of W (left by
+    // the previous K2 launch) -- a rare ~2e-4 full-size parity failure
+    __threadfence();
+    __syncwarp();
     if (lane == 0) {
       if (nonfinite) atomicOr(t.nonfinite, 1);
       if (phase == 0) t.degmask[L.deg_idx] = dmask;
