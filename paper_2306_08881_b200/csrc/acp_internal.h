@@ -243,7 +243,7 @@ cudaError_t launch_stream(int mode, int rt, const Tables& t, const StreamSeg* se
 cudaError_t launch_materialize(const Tables& t, const LayerDesc& L, int layer, float* dst,
                                cudaStream_t stream);
 // tt_override > 0: tile target (floats per tensor per stage) instead of the mode's default
-bool stream_make_map(int mode, int64_t m, int rt, StreamMap* out, int tt_override = 0);
+bool stream_make_map(int mode, int64_t m, int rt, StreamMap* out, int tt_override = 0, bool k1p2 = false);
 // Tensor-core K1 (k_tc.cu). mode 0: P-step (x = M + S - P_orth Q_loc^T,
 // S = x, P_loc = x Q_orth -> P slot + P_loc split), mode 1: Q-step
 // (x = M + S - P_loc Q_orth^T, S = x, Q partials = x^T P_orth -> colpart).

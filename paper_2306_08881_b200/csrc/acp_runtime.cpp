@@ -62,6 +62,7 @@ struct Plan {
   bool defer = false;   // deferred Q-step residual (stream kernels)
   bool psgd = false;    // ACP_POWERSGD: the Power-SGD baseline (NEXT-1)
   bool tc = false;      // tensor-core K1 + double-deferred residual
+  bool k1p2 = false;    // SIMT K1-P' on the two-row kernel (k_stream.cu k1p_kernel); ACP_K1P_OLD=1: seg_k1p
   bool bucketed = false;  // multi-rank scheduler (world_size > 1 or ACP_BUCKETED)
   bool tc5 = false;       // TC path decodes on tcgen05 / TMEM (k_tc5.cu); ACP_NO_TC5=1: mma.sync
   int R8 = 0;           // TC path: rank padded to a multiple of 8
@@ -213,6 +214,10 @@ acp_status build_plan(const acp_config* cfg, Plan& P, bool plan_only = false) {
   P.tc = P.ef && !P.psgd && P.RT <= 32 && !std::getenv("ACP_NO_TC") &&
          (P.RT >= 8 || (tc_env && std::atoi(tc_env) != 0));
   P.R8 = P.tc ? std::max(8, (P.RT + 7) / 8 * 8) : 0;
+  {
+    const char* e = std::getenv("ACP_K1P_OLD");
+    P.k1p2 = P.ef && !P.psgd && P.RT <= 4 && !(e && std::atoi(e) != 0);
+  }
   P.tc5 = P.tc && !std::getenv("ACP_NO_TC5");
   // tcgen05 K1 P-step: faster than the mma.sync kernel at r = 32 (BERT-L
   // proj_p 1.22 -> 1.09 ms), slower at r = 16 (0.93 -> 0.99) and r = 8
@@ -277,7 +282,8 @@ acp_status build_plan(const acp_config* cfg, Plan& P, bool plan_only = false) {
         // traffic at 100% of the copy peak with 3 x 64 KB stages)
         static const int wide_m = std::getenv("ACP_K1P_WIDE") ? std::atoi(std::getenv("ACP_K1P_WIDE")) : 4096;
         static const int wide_tt = std::getenv("ACP_K1P_WIDE_TT") ? std::atoi(std::getenv("ACP_K1P_WIDE_TT")) : 0;
-        stream_make_map(0, L.m, P.RT, &L.sm[0], (wide_m > 0 && L.m >= wide_m && P.RT <= 4) ? wide_tt : 0);
+        stream_make_map(0, L.m, P.RT, &L.sm[0], (wide_m > 0 && L.m >= wide_m && P.RT <= 4) ? wide_tt : 0,
+                        P.k1p2);
         // K1-P stages the layer's local Q (RT x m) next to two ring stages
         const StreamMap& m0 = L.sm[0];
         if (m0.tr > 0 && 4 * ((int64_t)P.RT * L.m + 4LL * m0.tr * m0.pcols + 2LL * m0.tr * P.RT) +
@@ -489,7 +495,7 @@ acp_status build_plan(const acp_config* cfg, Plan& P, bool plan_only = false) {
     stage_floats = (stage_floats + 31) / 32 * 32;
     const int cps = stream_ctas_per_sm(mode);
     // P rows per stage (modes 2, 3 always; mode 0 when deferred): [tr][RT]
-    const bool need_p = mode != 0 || P.defer;
+    const bool need_p = mode != 0 || (P.defer && !P.k1p2);  // k1p_kernel reads P_o from the slot
     // row stride RT in sP; the kernel derives it as ptile / tr per layer, so
     // size per-layer slots as tr_layer * RT and reserve max_tr * RT per stage
     ln.ptile = need_p ? (int)(max_tr * P.RT) : 0;
@@ -503,6 +509,7 @@ acp_status build_plan(const acp_config* cfg, Plan& P, bool plan_only = false) {
       smem_overflow = true;
     ln.defer = (P.defer && (mode == 0 || mode == 3)) ? 1 : 0;
     if (P.psgd && mode == 0) ln.defer = 2;  // projection only (no residual write)
+    if (P.k1p2 && mode == 0) ln.defer |= 4;  // two-row kernel (its own stream map)
     int64_t part = 0;
     int prev_layer = -1, prev_panel = -1;
     ln.red_off = (int64_t)P.redtasks.size();

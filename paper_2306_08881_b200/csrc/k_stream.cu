@@ -22,7 +22,9 @@
 // register budget, gradient not 16-byte aligned) run a generic path in the
 // same launch; vectors (1-D params) are packed/unpacked here too.
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
+#include <type_traits>
 #include <utility>
 #include <vector>
 
@@ -414,6 +416,17 @@ __device__ void seg_fast(const Tables& t, const LayerDesc& L, const StreamSeg& s
         const float4 b = lds4(tE + toff + coff[i]);
         x[i] = (rval && cval[i]) ? f4add(a, b) : zero4();
       }
+      // P row staged by the producer (zero beyond r): read BEFORE the stage
+      // is released -- the producer regathers the stage's P rows for a later
+      // tile as soon as every warp has arrived (reading it after the arrive
+      // was a rare cross-warp race: one warp's rows projected on the next
+      // tile's P rows, ~5e-4 on a Q factor panel)
+      float pk[RT];
+      if constexpr (MODE != 0) {
+        const float* ps = sh.sP + (size_t)stage * sh.ptile + (rval ? tri : 0) * (sh.ptile / TR);
+#pragma unroll
+        for (int k = 0; k < RT; ++k) pk[k] = ps[k];
+      }
       if (j == rs - 1) {
         __syncwarp();
         if (lane == 0) mbar_arrive(&sh.empty[stage]);
@@ -481,12 +494,6 @@ __device__ void seg_fast(const Tables& t, const LayerDesc& L, const StreamSeg& s
             if (k < r) t.pbuf[L.p_off + (int64_t)k * n + row] = acc[k];
         }
       } else {
-        float pk[RT];  // P row staged by the producer (zero beyond r)
-        {
-          const float* ps = sh.sP + (size_t)stage * sh.ptile + (rval ? tri : 0) * (sh.ptile / TR);
-#pragma unroll
-          for (int k = 0; k < RT; ++k) pk[k] = ps[k];
-        }
         if constexpr (MODE == 2) {
 #pragma unroll
           for (int i = 0; i < NC; ++i) {
@@ -785,11 +792,430 @@ __global__ void __launch_bounds__(nw_of(MODE, RT) * 32 + 32, Cfg<MODE>::CPS)
   }
 }
 
+// ---------------------------------------------------------------------------
+// K1 P-step at r <= 4, two rows per pass (k1p_kernel, the default for the
+// ACP P-step at r <= 4; ACP_K1P_OLD=1 selects stream_kernel<0> / seg_k1p).
+// Same tiles, ring and thread-to-column map as seg_k1p, with the per-row
+// overhead that made seg_k1p issue-bound (ncu: ~480 warp instructions per
+// row slot, 40 per element, of which 12 are the arithmetic) taken out:
+//  * the producer role is folded into consumer warp 0, which fills the ring
+//    at each tile start (two bulk copies per tile, from addresses cached
+//    per segment): 12 warps = 3 per SM sub-partition -> 168 registers
+//    instead of the 128 a 13th warp leaves, which pays for two rows in
+//    flight per warp;
+//  * the P_o rows of the deferred correction are not gathered into the
+//    ring by the producer (32 lanes of 4-byte cp.async per tile: with the
+//    1-row tiles of ResNet's wide layers that made warp 0 the bottleneck,
+//    every other warp waiting at the pass barrier -- 0.149 vs 0.101 ms)
+//    but loaded by the consumers from the P slot one pass ahead;
+//  * the 2*RT row sums of the two rows are reduced by a transposing
+//    butterfly (each level halves the values a lane carries: 2*RT - 1 +
+//    5 - log2(2*RT) shuffles instead of 5 * 2*RT), rows spread over gw warps
+//    take one named barrier per two rows, and the cross-warp sum is spread
+//    over the lanes that share a value;
+//  * the staged Q_loc columns of the deferred correction are loaded once
+//    for both rows, and the deferred / not-deferred loops are separate
+//    instantiations.
+// Measured (B200, A/B against ACP_K1P_OLD=1, same box): BERT-L r=4 K1-P'
+// 0.836 -> 0.689 ms (4.04 GB: 5.87 TB/s), ResNet-50 0.1015 -> 0.0825,
+// ResNet-152 0.218 -> 0.177. A variant with 8 consumer warps + a producer
+// warp (168 registers, up to 4 chunks per lane) spilled at r = 4 and left
+// ResNet's m = 4608 layers without a map (generic path): 0.75 ms.
+// ---------------------------------------------------------------------------
+constexpr int kK1pWarps = 12;
+
+// Ring producer state (warp 0; identical in its 32 lanes). The current
+// segment's addresses are cached here when the producer reaches it, so a
+// tile costs warp 0 no dependent descriptor loads (a 1-row tile of a
+// ResNet layer is only ~700 cycles of work for the CTA, and every warp
+// waits for warp 0 at the tile's pass barrier).
+struct Prod {
+  int si;            // segment of the next tile (a fast segment with rows left, or se)
+  int stage;
+  uint32_t phase;
+  int issued;        // tiles issued so far
+  int64_t r0, row1;  // next tile's first row, segment end
+  const float* gm;   // M row r0
+  const float* ge;   // E row r0
+  uint32_t rowb;     // bytes per row
+  int tr;
+};
+
+__device__ __forceinline__ void prod_seek(const Tables& t, const StreamSeg* segs, int se, Prod& pr) {
+  for (; pr.si < se; ++pr.si) {
+    const StreamSeg s = segs[pr.si];
+    const LayerDesc& L = t.layers[s.layer];
+    const float* grad = t.grads[s.layer];
+    if (!is_fast<0>(L, grad) || s.row0 >= s.row1) continue;
+    pr.r0 = s.row0;
+    pr.row1 = s.row1;
+    pr.gm = grad + s.row0 * L.m;
+    pr.ge = t.E + L.e_off + s.row0 * L.m;
+    pr.rowb = (uint32_t)(L.m * 4);
+    pr.tr = L.sm[0].tr;
+    return;
+  }
+}
+
+// Issue the next tile into pr.stage (its stage is known to be free): one
+// bulk copy per tensor (whole rows) by lane 0. (The P_o rows of the
+// deferred correction are not staged: the consumers load them from the P
+// slot one pass ahead.)
+__device__ __forceinline__ void prod_issue(const Tables& t, const StreamSeg* segs, int se,
+                                           const Shared& sh, Prod& pr, uint64_t pol) {
+  const int lane = threadIdx.x & 31;
+  const int tr = pr.tr;
+  const int64_t nr = (pr.row1 - pr.r0) < tr ? (pr.row1 - pr.r0) : tr;
+  if (lane == 0) {
+    uint64_t* full = &sh.full[pr.stage];
+    const uint32_t bytes = (uint32_t)nr * pr.rowb;
+    mbar_arrive_tx(full, 2 * bytes);
+    bulk_g2s(sh.sM + (size_t)pr.stage * sh.stage_floats, pr.gm, bytes, full, pol);
+    bulk_g2s(sh.sE + (size_t)pr.stage * sh.stage_floats, pr.ge, bytes, full, pol);
+  }
+  ++pr.issued;
+  if (++pr.stage == sh.stages) {
+    pr.stage = 0;
+    pr.phase ^= 1u;
+  }
+  pr.r0 += tr;
+  const int64_t adv = (int64_t)tr * (pr.rowb >> 2);
+  pr.gm += adv;
+  pr.ge += adv;
+  if (pr.r0 >= pr.row1) {
+    ++pr.si;
+    prod_seek(t, segs, se, pr);
+  }
+}
+
+// Warp 0 issues tiles while fewer than `upto` are issued; called at each
+// tile start with upto = tile + stages, i.e. it fills the ring. The last of
+// those tiles reuses the stage of the previous tile, so this waits until
+// every warp has released that one (in layers whose rows span several warps
+// the pass barrier has already ensured it). Issuing only what is free at
+// that moment collapses the lookahead to one tile whenever the warps drift
+// apart, and extra early refill attempts (right after the last pass's
+// cross-warp barrier) delay warp 0 at the next barrier: both measured
+// slower.
+__device__ __forceinline__ void produce(const Tables& t, const StreamSeg* segs, int se, const Shared& sh,
+                                        Prod& pr, int upto, bool block, uint64_t pol) {
+  const int lane = threadIdx.x & 31;
+  while (pr.si < se && pr.issued < upto) {
+    uint32_t ok = 1;
+    if (lane == 0) {
+      if (block) mbar_wait(&sh.empty[pr.stage], pr.phase ^ 1u);
+      else ok = mbar_test(&sh.empty[pr.stage], pr.phase ^ 1u) ? 1u : 0u;
+    }
+    ok = __shfl_sync(0xffffffffu, ok, 0);
+    if (!ok) break;
+    prod_issue(t, segs, se, sh, pr, pol);
+  }
+}
+
+template <int RT, int NC, bool DEFER>
+__device__ void seg_k1p2(const Tables& t, const StreamSeg* segs, int se, const LayerDesc& L,
+                         const StreamSeg& s, const Shared& sh, Pipe& pp, Prod& pr, int& consumed,
+                         int& rph, uint64_t pol) {
+  constexpr int NW = kK1pWarps;
+  const StreamMap mp = L.sm[0];
+  const int lg = mp.lg, gw = mp.gw, rs = mp.rs, TR = mp.tr;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int sub = warp % gw, wrow = warp / gw;
+  const int lgi = lane / lg, li = lane - lgi * lg;
+  const int rowslot = wrow * (32 / lg) + lgi;
+  const int NRS = (NW / gw) * (32 / lg);
+  const int m = (int)L.m;
+  const int n = (int)L.n;
+  const int r = L.r;
+  const int m4 = m >> 2;
+  const int cbase = sub * lg * NC + li;
+  int coff[NC];
+  bool cval[NC];
+#pragma unroll
+  for (int i = 0; i < NC; ++i) {
+    const int c = cbase + lg * i;
+    cval[i] = c < m4;
+    coff[i] = 4 * (cval[i] ? c : 0);
+  }
+  float4 qa[NC][RT];
+  {
+    const float* Qf = t.qbuf + L.q_off;
+#pragma unroll
+    for (int i = 0; i < NC; ++i)
+#pragma unroll
+      for (int k = 0; k < RT; ++k) qa[i][k] = (cval[i] && k < r) ? ld_f4(Qf + k * m + coff[i]) : zero4();
+  }
+  float* __restrict__ E = t.E + L.e_off;
+  float* __restrict__ Pw = t.pbuf + L.p_off;
+  if constexpr (DEFER) {
+    // stage this layer's local Q (k-major) for E_prev = S - P_o Q_loc^T
+    const float* Ql = t.qloc + L.ql_off;
+    cta_sync1<NW * 32>();  // previous segment's readers are done
+    for (int idx = threadIdx.x; idx < RT * m4; idx += NW * 32) {
+      const int k = idx / m4, c = idx - k * m4;
+      *reinterpret_cast<float4*>(sh.sQl + k * m + 4 * c) = k < r ? ld_f4(Ql + k * m + 4 * c) : zero4();
+    }
+    cta_sync1<NW * 32>();
+  }
+  // P_o rows of the deferred correction, straight from the P slot (which
+  // still holds P_o until this kernel overwrites the row with P_loc, after
+  // every warp of the row group has read it), loaded one pass ahead so the
+  // L2 latency overlaps the previous pass
+  float pn[2][RT];
+  auto load_po = [&](int64_t r0x, int jx) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t rw = r0x + rowslot + NRS * (jx + h);
+      const bool ok = (jx + h < rs) && (rw < s.row1);
+#pragma unroll
+      for (int k = 0; k < RT; ++k) pn[h][k] = (ok && k < r) ? __ldcg(Pw + (int64_t)k * n + rw) : 0.f;
+    }
+  };
+  if constexpr (DEFER) load_po(s.row0, 0);
+  for (int64_t r0 = s.row0; r0 < s.row1; r0 += TR) {
+    const int nr = (int)((s.row1 - r0) < TR ? (s.row1 - r0) : TR);
+    if (warp == 0) produce(t, segs, se, sh, pr, consumed + sh.stages, true, pol);
+    const int stage = pp.stage;
+    mbar_wait(&sh.full[stage], pp.phase);
+    const float* tM = sh.sM + (size_t)stage * sh.stage_floats;
+    const float* tE = sh.sE + (size_t)stage * sh.stage_floats;
+    // one pass over ROWS (2, or 1 for an odd tail) rows of the tile
+    auto pass = [&](auto rows_c, int j) {
+      constexpr int ROWS = decltype(rows_c)::value;
+      constexpr int V = ROWS * RT;                       // row sums carried
+      constexpr int LOGV = V == 1 ? 0 : (V == 2 ? 1 : (V == 4 ? 2 : 3));
+      constexpr int G = 32 >> LOGV;                      // lanes sharing one reduced value
+      int tri[ROWS], toff[ROWS];
+      bool rv[ROWS];
+      int64_t row[ROWS];
+#pragma unroll
+      for (int h = 0; h < ROWS; ++h) {
+        tri[h] = rowslot + NRS * (j + h);
+        rv[h] = tri[h] < nr;
+        toff[h] = (rv[h] ? tri[h] : 0) * m;
+        row[h] = r0 + tri[h];
+      }
+
+      float4 x[ROWS][NC];
+      float v[V];
+#pragma unroll
+      for (int q = 0; q < V; ++q) v[q] = 0.f;
+#pragma unroll
+      for (int i = 0; i < NC; ++i) {
+#pragma unroll
+        for (int h = 0; h < ROWS; ++h)
+          x[h][i] = f4add(lds4(tM + toff[h] + coff[i]), lds4(tE + toff[h] + coff[i]));
+        if constexpr (DEFER) {
+#pragma unroll
+          for (int k = 0; k < RT; ++k) {
+            const float4 ql = lds4(sh.sQl + k * m + coff[i]);  // shared by the rows
+#pragma unroll
+            for (int h = 0; h < ROWS; ++h) f4fma(x[h][i], -pn[h][k], ql);
+          }
+        }
+#pragma unroll
+        for (int h = 0; h < ROWS; ++h)
+#pragma unroll
+          for (int k = 0; k < RT; ++k) {
+            float& a = v[h * RT + k];
+            a = fmaf(x[h][i].x, qa[i][k].x, a);
+            a = fmaf(x[h][i].y, qa[i][k].y, a);
+            a = fmaf(x[h][i].z, qa[i][k].z, a);
+            a = fmaf(x[h][i].w, qa[i][k].w, a);
+          }
+      }
+      if constexpr (DEFER) {
+        // P_o of the next pass (the next row pair of this tile, else the
+        // next tile's first), in flight during this pass's reduction
+        if (j + 2 < rs) load_po(r0, j + 2);
+        else if (r0 + TR < s.row1) load_po(r0 + TR, 0);
+      }
+      if (j + ROWS >= rs) {  // the tile's last pass: release the stage
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sh.empty[stage]);
+      }
+      float tot[V];
+      if (lg == 32) {
+        // transposing butterfly: at the level with offset 16 >> l a lane
+        // hands half of its values to its partner and keeps the other half
+        // (lane bit 4 - l picks which), until one value is left; the last
+        // 5 - LOGV levels are a plain butterfly on that value
+#pragma unroll
+        for (int lev = 0; lev < 5; ++lev) {
+          const int off = 16 >> lev;
+          const int w = lev < LOGV ? (V >> lev) : 1;
+          if (w > 1) {
+            const bool up = (lane & off) != 0;
+            const int hw = w >> 1;
+#pragma unroll
+            for (int q = 0; q < hw; ++q) {
+              const float send = up ? v[q] : v[q + hw];
+              const float keep = up ? v[q + hw] : v[q];
+              v[q] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+            }
+          } else {
+            v[0] += __shfl_xor_sync(0xffffffffu, v[0], off);
+          }
+        }
+        const int qi = LOGV == 0 ? 0 : ((lane >> (5 - LOGV)) & (V - 1));  // this lane's row sum
+        if (gw > 1) {
+          float* buf = sh.red + (rph & 1) * (16 * 8);
+          ++rph;
+          if ((lane & (G - 1)) == 0) buf[warp * 8 + qi] = v[0];
+          cta_sync1<NW * 32>();
+          float sum = 0.f;
+          for (int w = lane & (G - 1); w < gw; w += G) sum += buf[(wrow * gw + w) * 8 + qi];
+#pragma unroll
+          for (int off = 1; off < G; off <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+          v[0] = sum;
+        }
+        if (sub == 0 && (lane & (G - 1)) == 0) {
+          const int h = qi / RT, k = qi - h * RT;
+          int64_t rw = row[0];  // row[h] without a local-memory array
+          bool ok = rv[0];
+#pragma unroll
+          for (int hh = 1; hh < ROWS; ++hh)
+            if (h == hh) {
+              rw = row[hh];
+              ok = rv[hh];
+            }
+          if (k < r && ok) Pw[(int64_t)k * n + rw] = v[0];
+        }
+#pragma unroll
+        for (int q = 0; q < V; ++q) tot[q] = __shfl_sync(0xffffffffu, v[0], q << (5 - LOGV));
+      } else {
+        for (int off = lg >> 1; off > 0; off >>= 1)
+#pragma unroll
+          for (int q = 0; q < V; ++q) v[q] += __shfl_xor_sync(0xffffffffu, v[q], off);
+#pragma unroll
+        for (int q = 0; q < V; ++q) tot[q] = v[q];
+        if (li == 0) {
+#pragma unroll
+          for (int h = 0; h < ROWS; ++h)
+#pragma unroll
+            for (int k = 0; k < RT; ++k)
+              if (k < r && rv[h]) Pw[(int64_t)k * n + row[h]] = tot[h * RT + k];
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < ROWS; ++h) {
+        float* __restrict__ er = E + row[h] * m;
+#pragma unroll
+        for (int i = 0; i < NC; ++i) {
+          float4 a = x[h][i];
+#pragma unroll
+          for (int k = 0; k < RT; ++k) f4fma(a, -tot[h * RT + k], qa[i][k]);
+          if (rv[h] && cval[i]) st_cs4(er + coff[i], a);
+        }
+      }
+    };
+    int j = 0;
+    for (; j + 2 <= rs; j += 2) pass(std::integral_constant<int, 2>{}, j);
+    if (j < rs) pass(std::integral_constant<int, 1>{}, j);
+    pp.advance(sh.stages);
+    ++consumed;
+  }
+}
+
+__device__ __forceinline__ Shared make_shared(unsigned char* smem_raw, int stages, int stage_floats,
+                                              int factor_floats, int ptile) {
+  Shared sh;
+  sh.stages = stages;
+  sh.stage_floats = stage_floats;
+  sh.sM = reinterpret_cast<float*>(smem_raw);
+  sh.sE = sh.sM + (size_t)stages * stage_floats;
+  sh.full = reinterpret_cast<uint64_t*>(sh.sE + (size_t)stages * stage_floats);
+  sh.empty = sh.full + stages;
+  sh.red = reinterpret_cast<float*>(sh.empty + stages);
+  sh.gred = sh.red + 2 * 16 * 8;
+  sh.cred = reinterpret_cast<float4*>(sh.gred + 16 * 32);
+  sh.sQl = reinterpret_cast<float*>(sh.cred + 16 * 32);
+  sh.sP = sh.sQl + factor_floats;
+  sh.ptile = ptile;
+  sh.flag = reinterpret_cast<int*>(sh.sP + (size_t)stages * ptile);
+  return sh;
+}
+
+template <int RT>
+__global__ void __launch_bounds__(kK1pWarps * 32, 1)
+    k1p_kernel(Tables t, const StreamSeg* __restrict__ segs, const int32_t* __restrict__ cta_begin,
+               int stages, int stage_floats, int factor_floats, int defer, int ptile) {
+  constexpr int NT = kK1pWarps * 32;
+  static_assert(nw_of(0, RT) == kK1pWarps, "k1p_kernel shares the 12-warp stream map");
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const Shared sh = make_shared(smem_raw, stages, stage_floats, factor_floats, ptile);
+  const int dflag = (defer & 1) ? *t.deferred : 0;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < stages; ++i) {
+      mbar_init(&sh.full[i], 1);
+      mbar_init(&sh.empty[i], kK1pWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int sb = cta_begin[blockIdx.x], se = cta_begin[blockIdx.x + 1];
+  prefetch_segs(t, segs, sb, se);
+  const uint64_t pol = policy_evict_first();
+  Prod pr{};
+  pr.si = sb;
+  Pipe pp;
+  int consumed = 0, rph = 0;
+  if ((threadIdx.x >> 5) == 0) {  // the first tiles go out before any other work
+    prod_seek(t, segs, se, pr);
+    produce(t, segs, se, sh, pr, sh.stages, true, pol);
+  }
+  for (int si = sb; si < se; ++si) {
+    if (!t.layers[segs[si].layer].mat) {
+      si = vector_run(t, segs, si, se, threadIdx.x >> 5, NT / 32,
+                      [&](const StreamSeg& s, const LayerDesc& L, int first, int stride) {
+                        const float* grad = t.grads[s.layer];
+                        float* slot = t.pbuf + L.p_off;
+                        for (int64_t i = s.row0 + first; i < s.row1; i += stride) slot[i] = grad[i];
+                      }) - 1;
+      continue;
+    }
+    const StreamSeg s = segs[si];
+    const LayerDesc& L = t.layers[s.layer];
+    float* grad = t.grads[s.layer];
+    if (!is_fast<0>(L, grad)) {
+      seg_generic<0, RT>(t, L, s, grad, 1.0f, sh.gred, dflag);
+      continue;
+    }
+    switch (L.sm[0].nc) {
+#define ACP_CASE(NCV)                                                                          \
+  case NCV:                                                                                    \
+    if (dflag) seg_k1p2<RT, NCV, true>(t, segs, se, L, s, sh, pp, pr, consumed, rph, pol); \
+    else seg_k1p2<RT, NCV, false>(t, segs, se, L, s, sh, pp, pr, consumed, rph, pol);     \
+    break;
+      ACP_CASE(1)
+      ACP_CASE(2)
+      ACP_CASE(3)
+#undef ACP_CASE
+      default: break;
+    }
+  }
+}
+
 template <int MODE>
 cudaError_t launch_mode(int rt, const Tables& t, const StreamSeg* segs, const int32_t* cb, int ncta,
                         float scale, int stages, int stage_floats, int factor_floats, int defer,
                         int ptile, cudaStream_t st) {
   const size_t smem = stream_smem_bytes(stages, stage_floats, factor_floats, ptile);
+  // K1 P-step on the two-row kernel (defer bit 2, set by the plan)
+  if (MODE == 0 && rt <= 4 && (defer & 4)) {
+    auto go2 = [&](auto kern) -> cudaError_t {
+      cudaError_t e = allow_max_smem(reinterpret_cast<const void*>(kern));
+      if (e != cudaSuccess) return e;
+      kern<<<ncta, kK1pWarps * 32, smem, st>>>(t, segs, cb, stages, stage_floats, factor_floats, defer, ptile);
+      return cudaGetLastError();
+    };
+    switch (rt) {
+      case 1: return go2(k1p_kernel<1>);
+      case 2: return go2(k1p_kernel<2>);
+      case 4: return go2(k1p_kernel<4>);
+      default: break;
+    }
+  }
   auto go = [&](auto kern) -> cudaError_t {
     cudaError_t e = allow_max_smem(reinterpret_cast<const void*>(kern));
     if (e != cudaSuccess) return e;
@@ -917,7 +1343,8 @@ int stream_ctas_per_sm(int mode) {
   return mode == 0 ? Cfg<0>::CPS : (mode == 2 ? Cfg<2>::CPS : Cfg<3>::CPS);
 }
 
-bool stream_make_map(int mode, int64_t m, int rt, StreamMap* out, int tt_override) {
+bool stream_make_map(int mode, int64_t m, int rt, StreamMap* out, int tt_override, bool k1p2) {
+  (void)k1p2;  // k1p_kernel uses seg_k1p's 12-warp geometry
   *out = StreamMap{};
   if (m % 4 != 0 || rt > 8) return false;
   const int NW = nw_of(mode, rt);
