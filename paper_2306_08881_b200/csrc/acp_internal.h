@@ -10,6 +10,7 @@ namespace acp {
 constexpr int kThreads = 256;          // every hot kernel runs 256-thread CTAs
 constexpr int kMaxV = 8;               // row kernel: float4 chunks per thread per row
 constexpr int kOrthRowsPerSeg = 256;   // K2 work unit (factor rows), staged at once
+constexpr int kOrthLocalFloats = 18432;  // K2: factors with r * len <= this (r <= 8) run in one CTA
 constexpr int kOrthRowsPerSegLarge = 1024;  // K2 unit at rank <= 2 (<= 4 forced) when a phase has
                                            // >= one item per SM (fewer queue rounds)
 
@@ -121,6 +122,8 @@ struct OrthSeg {
   int64_t gram_off;    // double offset of this segment's partial Gram (r x r)
   int32_t nseg;        // segments of this layer
   int32_t gram_first;  // segment index of the layer's first partial (gram_off of seg 0)
+  int32_t local;       // 1: the whole factor in one CTA (orth_local), nseg = 1
+  int32_t pad_;
 };
 
 // K1 Q-step second stage: one (layer, panel) output unit. Items

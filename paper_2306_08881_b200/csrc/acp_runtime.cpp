@@ -804,14 +804,26 @@ acp_status build_plan(const acp_config* cfg, Plan& P, bool plan_only = false) {
     if (seg_env && P.RT <= 4) large = std::atoi(seg_env) == kOrthRowsPerSegLarge;
     P.orth_seg[side] = large ? kOrthRowsPerSegLarge : kOrthRowsPerSeg;
   }
+  // Small factors (r <= 8, r * len <= kOrthLocalFloats) run whole in one CTA
+  // (orth_local: no cross-CTA phases); they follow the segmented layers'
+  // items in the queue, largest first. ACP_ORTH_LOCAL=0 disables it.
+  const char* loc_env = std::getenv("ACP_ORTH_LOCAL");  // 0: off; else the r * len threshold
+  const int64_t loc_max = loc_env ? std::min<int64_t>(std::atoll(loc_env), kOrthLocalFloats) : kOrthLocalFloats;
+  const bool orth_local = P.RT <= 8 && loc_max > 0;
   for (int side = 0; side < 2; ++side) {
     int64_t g = 0;
     double bytes = 0;
     const int64_t segr = P.orth_seg[side];
+    std::vector<std::pair<int64_t, int>> locals;
     for (int i = 0; i < P.T; ++i) {
       const LayerDesc& L = P.L[i];
       if (!L.mat) continue;
       const int64_t len = side == 0 ? L.m : L.n;
+      bytes += 4.0 * L.r * (double)len * 5.0;  // read, read+write, read+write
+      if (orth_local && (int64_t)L.r * len <= loc_max) {
+        locals.emplace_back(-len, i);
+        continue;
+      }
       const int nseg = (int)((len + segr - 1) / segr);
       for (int j = 0; j < nseg; ++j) {
         OrthSeg s{};
@@ -824,7 +836,16 @@ acp_status build_plan(const acp_config* cfg, Plan& P, bool plan_only = false) {
         g += (int64_t)L.r * L.r;
         P.orthsegs[side].push_back(s);
       }
-      bytes += 4.0 * L.r * (double)len * 5.0;  // read, read+write, read+write
+    }
+    std::stable_sort(locals.begin(), locals.end());
+    for (const auto& lc : locals) {
+      OrthSeg s{};
+      s.layer = lc.second;
+      s.row0 = 0;
+      s.row1 = -lc.first;
+      s.nseg = 1;
+      s.local = 1;
+      P.orthsegs[side].push_back(s);
     }
     P.gram_elems = std::max<int64_t>(P.gram_elems, g);
     P.orth_bytes[side] = bytes;

@@ -25,7 +25,12 @@ constexpr double kDegTol2 = 1e-12;      // (1e-6)^2, reading C6
 template <int RT, int SEG>
 constexpr size_t orth_smem() {
   constexpr int kLd = SEG + 1;
-  return (size_t)2 * RT * kLd * 4 + (size_t)3 * RT * RT * 8 + kThreads * 8 + 16;
+  const size_t seg = (size_t)2 * RT * kLd * 4 + (size_t)3 * RT * RT * 8 + kThreads * 8 + 16;
+  // orth_local: [r][len] floats + Gs / Rm / Wm + per-warp pair sums + mask
+  const size_t loc = RT > 8 ? 0
+                            : (size_t)4 * ((kOrthLocalFloats + 3) & ~3) + (size_t)3 * RT * RT * 8 +
+                                  (size_t)(kThreads / 32) * (RT * (RT + 1) / 2) * 8 + 32;
+  return seg > loc ? seg : loc;
 }
 
 // Layer `s.layer`'s phase `phase` may start once lflag[layer] >= ready_epoch
@@ -113,6 +118,55 @@ __device__ __noinline__ void chol_inv_regs(const Tables& t, const LayerDesc& L, 
     // publish: the layer's next phase may start
     *reinterpret_cast<volatile long long*>(t.orthflag + L.deg_idx) = orth_epoch(step, phase + 1);
   }
+}
+
+// Cholesky G = R^T R (R upper) and W = R^-1 of one layer's r x r Gram (r <=
+// 32) by one warp, lane l owning column l (left-looking; shared memory). A
+// degenerate column (residual <= 1e-6 of its norm) is dropped (C6): its row
+// and column of R are zero, R_kk = 1, and W_kk = 0 (its output column is
+// replaced by the seeded Gaussian one). A non-finite column is NOT repaired
+// (non-finite input is an error): it propagates NaN and is
+// reported through `nonfinite`. Out: Rm, Wm (r x r, row-major, W upper
+// triangular with zeros below), dmask (bit k: column k dropped).
+__device__ __forceinline__ void chol_small(const double* Gs, double* Rm, double* Wm, int r,
+                                           uint32_t& dmask, bool& nonfinite) {
+  const int lane = threadIdx.x & 31;
+  for (int k = 0; k < r; ++k) {
+    const double gkk = Gs[k * r + k];
+    double d = gkk;
+    for (int j = 0; j < k; ++j) {
+      const double rjk = Rm[j * r + k];
+      d = fma(-rjk, rjk, d);
+    }
+    const bool fin = isfinite(gkk);
+    nonfinite |= !fin;
+    const bool dg = fin && (!(gkk > 0.0) || !(d > kDegTol2 * gkk));
+    const double rkk = dg ? 1.0 : sqrt(d);
+    if (dg) dmask |= 1u << k;
+    if (lane < r) {
+      if (dg) {
+        if (lane < k) Rm[lane * r + k] = 0.0;
+        else if (lane > k) Rm[k * r + lane] = 0.0;
+      } else if (lane > k) {
+        double v = Gs[k * r + lane];
+        for (int j = 0; j < k; ++j) v = fma(-Rm[j * r + k], Rm[j * r + lane], v);
+        Rm[k * r + lane] = v / rkk;
+      }
+      if (lane == k) Rm[k * r + k] = rkk;
+    }
+    __syncwarp();
+  }
+  if (lane < r) {
+    const int l = lane;  // back substitution for column l of W
+    for (int i = l; i >= 0; --i) {
+      double v = (i == l) ? 1.0 : 0.0;
+      for (int j = i + 1; j <= l; ++j) v = fma(-Rm[i * r + j], Wm[j * r + l], v);
+      Wm[i * r + l] = v / Rm[i * r + i];
+    }
+    if ((dmask >> l) & 1u) Wm[l * r + l] = 0.0;
+    for (int i = l + 1; i < r; ++i) Wm[i * r + l] = 0.0;
+  }
+  __syncwarp();
 }
 
 // One (phase, segment) work item of K2. Returns after the item; the layer's
@@ -307,50 +361,11 @@ __device__ void orth_item(const Tables& t, int side, const OrthSeg& s, int phase
     const int lane = tid;
     uint32_t dmask = 0;
     bool nonfinite = false;
-    // left-looking Cholesky G = R^T R (R upper), lane l owns column l;
-    // a degenerate column (residual <= 1e-6 of its norm) is dropped (C6).
-    // A non-finite column is NOT repaired (non-finite input is an
-    // error): it propagates NaN and raises the sticky flag for the host.
-    for (int k = 0; k < r; ++k) {
-      const double gkk = Gs[k * r + k];
-      double d = gkk;
-      for (int j = 0; j < k; ++j) {
-        const double rjk = Rm[j * r + k];
-        d = fma(-rjk, rjk, d);
-      }
-      const bool fin = isfinite(gkk);
-      nonfinite |= !fin;
-      const bool dg = fin && (!(gkk > 0.0) || !(d > kDegTol2 * gkk));
-      const double rkk = dg ? 1.0 : sqrt(d);
-      if (dg) dmask |= 1u << k;
-      if (lane < r) {
-        if (dg) {
-          if (lane < k) Rm[lane * r + k] = 0.0;
-          else if (lane > k) Rm[k * r + lane] = 0.0;
-        } else if (lane > k) {
-          double v = Gs[k * r + lane];
-          for (int j = 0; j < k; ++j) v = fma(-Rm[j * r + k], Rm[j * r + lane], v);
-          Rm[k * r + lane] = v / rkk;
-        }
-        if (lane == k) Rm[k * r + k] = rkk;
-      }
-      __syncwarp();
-    }
-    // W = R^-1 (upper triangular), lane l solves column l; W_kk = 0 for a
-    // dropped column (its output column is replaced by a seeded one)
+    chol_small(Gs, Rm, Wm, r, dmask, nonfinite);
     double* Wout = phase == 0 ? W1 : W2;
     if (lane < r) {
       const int l = lane;
-      for (int i = l; i >= 0; --i) {
-        double v = (i == l) ? 1.0 : 0.0;
-        for (int j = i + 1; j <= l; ++j) v = fma(-Rm[i * r + j], Wm[j * r + l], v);
-        Wm[i * r + l] = v / Rm[i * r + i];
-      }
-      for (int i = 0; i < r; ++i) {
-        double w = i <= l ? Wm[i * r + l] : 0.0;
-        if (((dmask >> l) & 1u) && i == l) w = 0.0;
-        Wout[i * r + l] = w;
-      }
+      for (int i = 0; i < r; ++i) Wout[i * r + l] = Wm[i * r + l];
     }
     // every lane's W columns must be visible GPU-wide before lane 0 publishes
     // the flag the next phase's items (other SMs) wait on: without this, lane
@@ -369,6 +384,142 @@ __device__ void orth_item(const Tables& t, int side, const OrthSeg& s, int phase
     }
   }
   __syncthreads();
+}
+
+// K2 of one whole small factor (r * len <= kOrthLocalFloats, r <= 8) in one
+// CTA: the same three CholeskyQR2 steps as orth_item, with __syncthreads
+// between them instead of the cross-CTA epoch flags and partial Grams (a
+// ResNet layer's three phases otherwise cost three queue rounds and two
+// flag hand-offs for a few microseconds of arithmetic). Same arithmetic per
+// element: fp64 Gram of the fp32 rows, fp64 apply rounded to fp32, the
+// degenerate-column rule (C6) on the first Cholesky only.
+template <int RT>
+__device__ void orth_local(const Tables& t, int side, const OrthSeg& s, uint64_t seed, int64_t step,
+                           unsigned char* smem_raw) {
+  constexpr int NP = RT * (RT + 1) / 2;
+  constexpr int NWP = kThreads / 32;
+  const LayerDesc L = t.layers[s.layer];
+  const int r = L.r;
+  const int len = (int)(side == 0 ? L.m : L.n);
+  float* F = side == 0 ? t.qbuf + L.q_off : t.pbuf + L.p_off;  // k-major [r][len]
+  float* A = reinterpret_cast<float*>(smem_raw);                 // [r][len]
+  double* Gs = reinterpret_cast<double*>(smem_raw + 4 * ((kOrthLocalFloats + 3) & ~3));
+  double* Rm = Gs + RT * RT;
+  double* Wm = Rm + RT * RT;
+  double* red = Wm + RT * RT;                                    // [NWP][NP]
+  uint32_t* dsh = reinterpret_cast<uint32_t*>(red + NWP * NP);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int total = r * len;
+  // stage the factor (contiguous k-major [r][len]) with ONE bulk copy: an
+  // item of 4608 x 4 spent ~15k cycles in 18 rounds of dependent 4-byte
+  // loads. The size is rounded up to 16 bytes (the arena slots are 16-byte
+  // aligned and padded, so the tail stays inside the arena).
+  {
+    uint64_t* bar = reinterpret_cast<uint64_t*>(dsh + 2);
+    const uint32_t bytes = (uint32_t)(((total + 3) & ~3) * 4);
+    if (tid == 0) {
+      mbar_init(bar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      fence_async_smem();  // generic-proxy writes to A by the previous item
+      mbar_arrive_tx(bar, bytes);
+      bulk_g2s(A, F, bytes, bar, policy_evict_first());
+    }
+    __syncthreads();
+    mbar_wait(bar, 0);
+  }
+  bool nonfinite = false;
+  uint32_t deg = 0;
+  for (int pass = 0; pass < 2; ++pass) {
+    // Gram of the current rows (fp64): rows strided over the threads, all
+    // pairs (k <= l) per thread, then a fixed-order warp / CTA reduction
+    double g[NP];
+#pragma unroll
+    for (int p = 0; p < NP; ++p) g[p] = 0.0;
+    for (int i = tid; i < len; i += kThreads) {
+      double a[RT];
+#pragma unroll
+      for (int k = 0; k < RT; ++k) a[k] = k < r ? (double)A[k * len + i] : 0.0;
+#pragma unroll
+      for (int k = 0, p = 0; k < RT; ++k)
+#pragma unroll
+        for (int l = 0; l <= k; ++l, ++p) g[p] = fma(a[k], a[l], g[p]);
+    }
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) g[p] += __shfl_xor_sync(0xffffffffu, g[p], off);
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int p = 0; p < NP; ++p) red[warp * NP + p] = g[p];
+    }
+    __syncthreads();
+    for (int p = tid; p < NP; p += kThreads) {
+      int k = 0;
+      while ((k + 1) * (k + 2) / 2 <= p) ++k;
+      const int l = p - k * (k + 1) / 2;
+      double v = 0.0;
+      for (int w = 0; w < NWP; ++w) v += red[w * NP + p];
+      if (k < r && l < r) {
+        Gs[k * r + l] = v;
+        Gs[l * r + k] = v;
+      }
+    }
+    for (int i = tid; i < r * r; i += kThreads) Rm[i] = 0.0;
+    __syncthreads();
+    if (warp == 0) {
+      uint32_t dmask = 0;
+      chol_small(Gs, Rm, Wm, r, dmask, nonfinite);
+      if (lane == 0 && pass == 0) *dsh = dmask;
+    }
+    __syncthreads();
+    if (pass == 0) deg = *dsh;
+    // apply W (upper triangular), thread per row: out_l = sum_{k<=l} a_k W_kl;
+    // after the first Cholesky a dropped column becomes the seeded Gaussian
+    // column (reading C6); the second apply's output is the factor
+    for (int i = tid; i < len; i += kThreads) {
+      double a[RT];
+#pragma unroll
+      for (int k = 0; k < RT; ++k) a[k] = k < r ? (double)A[k * len + i] : 0.0;
+#pragma unroll
+      for (int l = 0; l < RT; ++l) {
+        if (l >= r) break;
+        double v = 0.0;
+        if (pass == 0 && ((deg >> l) & 1u)) {
+          v = (double)gaussian_at(column_key(seed, kTagDegenerate, (uint64_t)s.layer, (uint64_t)step,
+                                             (uint64_t)l),
+                                  (uint64_t)i);
+        } else {
+#pragma unroll
+          for (int k = 0; k <= l; ++k) v = fma(a[k], Wm[k * r + l], v);
+        }
+        const float vf = (float)v;
+        if (pass == 0) {
+          A[l * len + i] = vf;  // this thread's row only: read above, in place
+        } else {
+          F[(int64_t)l * len + i] = vf;
+          if (t.r8 > 0) {  // TC path split copies (as orth_item's phase 2)
+            uint32_t hi, lo;
+            split_tf32(vf, hi, lo);
+            const int64_t row = i, R8 = t.r8;
+            if (side == 0) {
+              float* d = t.qsplit + L.qs_off;
+              d[l * len + row] = __uint_as_float(hi);
+              d[(R8 + l) * len + row] = __uint_as_float(lo);
+            } else {
+              float* d = t.psplit + L.ps_off;
+              d[row * R8 + l] = __uint_as_float(hi);
+              d[(len + row) * R8 + l] = __uint_as_float(lo);
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (warp == 0) {
+    if (__any_sync(0xffffffffu, nonfinite) && lane == 0) atomicOr(t.nonfinite, 1);
+  }
 }
 
 // K2 as one persistent launch: CTAs take (phase, segment) items from a queue
@@ -392,7 +543,14 @@ __global__ void __launch_bounds__(kThreads) orth_kernel(Tables t, int side,
     __syncthreads();
     if (it >= total) break;
     const int phase = it / nseg;
-    orth_item<RT, SEG>(t, side, segs[it - phase * nseg], phase, seed, step, orth_smem_raw);
+    const OrthSeg& sg = segs[it - phase * nseg];
+    if (sg.local) {  // whole small factor in this CTA (phase-0 pass only)
+      if constexpr (RT <= 8) {
+        if (phase == 0) orth_local<RT>(t, side, sg, seed, step, orth_smem_raw);
+      }
+      continue;
+    }
+    orth_item<RT, SEG>(t, side, sg, phase, seed, step, orth_smem_raw);
   }
   if (threadIdx.x == 0) {
     __threadfence();
