@@ -14,7 +14,7 @@ rm -f gpurun_out/*.ncu-rep
 for W in bert-large-r4 resnet50-r4 bert-large-r32 bert-large-r8; do
   SMALL="bench.py --workload $W --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-powersgd --secondary none"
   timeout 300 python $SMALL > gpurun_out/bench_small_${TAG}_$W.log 2>&1 && \
-  timeout 1200 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"stream_kernel|row_kernel|orth_kernel|col_reduce|tc_kernel|tc5_" -s 8 -c 9 -o gpurun_out/prof_${TAG}_$W python $SMALL > gpurun_out/ncu_full_${TAG}_$W.log 2>&1; echo ncu_${W}_rc=$?
+  timeout 1200 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"stream_kernel|k1p_kernel|row_kernel|orth_kernel|col_reduce|tc_kernel|tc5_" -s 8 -c 9 -o gpurun_out/prof_${TAG}_$W python $SMALL > gpurun_out/ncu_full_${TAG}_$W.log 2>&1; echo ncu_${W}_rc=$?
   python scripts/traffic_from_ncu.py gpurun_out/prof_${TAG}_$W.ncu-rep $W $TAG
   python scripts/summarize_ncu.py full gpurun_out/prof_${TAG}_$W.ncu-rep gpurun_out/${TAG}_ncu_full_$W.md > /dev/null
   # only gpurun_out/ comes back (<= 64 MiB): keep the json and the summaries

@@ -47,7 +47,7 @@ def launches(path, out):
         k = short(r["Kernel Name"])
         tot[k] += v * scale
         cnt[k] += 1
-    ours = {k: v for k, v in tot.items() if any(s in k for s in ("row_kernel", "col_kernel", "orth_kernel", "stream_", "fill_kernel", "tc_kernel", "tc5_", "col_reduce", "finite_scan"))}
+    ours = {k: v for k, v in tot.items() if any(s in k for s in ("row_kernel", "col_kernel", "orth_kernel", "stream_", "k1p_kernel", "fill_kernel", "tc_kernel", "tc5_", "col_reduce", "finite_scan", "nvls", "materialize", "transpose"))}
     all_t = sum(tot.values())
     our_t = sum(ours.values())
     with open(out, "w") as f:

@@ -32,7 +32,7 @@ def kclass(name):
     m = re.search(r"row_kernel<\(int\)(\d)", n) or re.search(r"row_kernel<(\d)", n)
     if m:
         return {"0": "proj_p", "1": "decode_p", "2": "decode_q", "3": "decode_q"}[m.group(1)]
-    if "tc5_k1p" in n:
+    if "tc5_k1p" in n or "k1p_kernel" in n:
         return "proj_p"
     m = re.search(r"tc5_decode_kernel<\(int\)(\d)", n) or re.search(r"tc5_decode_kernel<(\d)", n)
     if m:
