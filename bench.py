@@ -469,7 +469,7 @@ def run_ours(args):
                      "gpu_launches": s["launches"]}
         s["ctx"].close()
     psgd = None
-    if not args.no_powersgd and r <= 8:
+    if not args.no_powersgd:
         # NEXT-1 / NEXT-4 context: the Power-SGD baseline (two projections and
         # two all-reduces per step) through the same library
         from paper_2306_08881_b200 import ACP_POWERSGD

@@ -109,7 +109,7 @@ enum {
                          split API acp_compress(0) forms P (no orthogonalisation),
                          acp_compress(1) orthogonalises the reduced P and forms
                          Q, acp_decompress(1) decodes (acp_decompress(0) is a
-                         no-op). Needs error feedback and rank <= 8; not
+                         no-op). Needs error feedback; not
                          combinable with ACP_NO_EF / ACP_NO_REUSE            */
   ACP_BUCKETED = 16u, /* run the multi-rank scheduler (compute groups, the comm
                          stream, one NCCL all-reduce per bucket inside an NCCL

@@ -351,7 +351,8 @@ acp_status build_plan(const acp_config* cfg, Plan& P, bool plan_only = false) {
         bytes += 8.0 * L.n;
         continue;
       }
-      const double bpe = mode == 0 ? (ef ? 12.0 : 4.0) : ((mode == 1 || mode == 3) ? 4.0 : (ef ? 16.0 : 8.0));
+      const double bpe = mode == 0 ? (ef ? (P.psgd ? 8.0 : 12.0) : 4.0)
+                                   : ((mode == 1 || mode == 3) ? 4.0 : (ef ? 16.0 : 8.0));
       int64_t align = 1;
       if (L.G > 0) align = (int64_t)(kThreads / L.G) * row_rows_per_iter(mode, L.V, P.RT);
       // balance by expected time, not bytes: the generic path is several
@@ -560,8 +561,10 @@ acp_status build_plan(const acp_config* cfg, Plan& P, bool plan_only = false) {
   // the deferred Q-step residual needs the stream kernels' layouts; the
   // environment switch keeps the 24-B/element Q-step for comparison
   P.defer = use_stream && !P.psgd && !P.tc && !std::getenv("ACP_NO_DEFER");
-  if (P.psgd && !use_stream)
-    return fail(ACP_E_INVAL, "ACP_POWERSGD needs error feedback and rank <= 8");
+  // Power-SGD: the SIMT stream kernels at r <= 8, the register row / column
+  // kernels above (projection-only row kernel, column kernel, row decode
+  // with the residual): 32 B / element either way
+  if (P.psgd && !P.ef) return fail(ACP_E_INVAL, "ACP_POWERSGD needs error feedback");
   // tensor-core K1 launch (mode 0 P-step, 1 Q-step) over `tensors`
   auto tc_launch = [&](int mode, const std::vector<int>& tensors) {
     if (mode >= 2 && P.tc5) {
@@ -1036,8 +1039,9 @@ acp_status run_k1(acp_ctx* c, int parity, const Launch& ln, cudaStream_t s) {
       ++c->launches;
     }
   }
-  else if (parity == 0)
-    e = launch_row(0, c->P.RT, c->tab, dev_rowsegs(c, ln), dev_ctab(c, ln), ln.ncta, 1.0f, ef, s);
+  else if (parity == 0)  // Power-SGD at r > 8: projection only (ef = 3)
+    e = launch_row(0, c->P.RT, c->tab, dev_rowsegs(c, ln), dev_ctab(c, ln), ln.ncta, 1.0f,
+                   (ef && c->P.psgd) ? 3 : ef, s);
   else
     e = launch_col(c->P.RT, c->tab, dev_colsegs(c, ln), dev_ctab(c, ln), ln.ncta, ef, s);
   prof_end(r, s);

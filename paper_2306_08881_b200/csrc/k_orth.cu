@@ -169,6 +169,13 @@ __device__ __forceinline__ void chol_small(const double* Gs, double* Rm, double*
   __syncwarp();
 }
 
+// The seeded Gaussian entry that replaces column l of a factor whose
+// column l was dropped (reading C6); out of line (rare path, large body).
+__device__ __noinline__ double degenerate_value(uint64_t seed, int layer, int64_t step, int l, int64_t row) {
+  return (double)gaussian_at(column_key(seed, kTagDegenerate, (uint64_t)layer, (uint64_t)step, (uint64_t)l),
+                             (uint64_t)row);
+}
+
 // One (phase, segment) work item of K2. Returns after the item; the layer's
 // last segment of phases 0 / 1 also computes W1 / W2 and publishes the
 // layer's next phase through lflag.
@@ -223,7 +230,75 @@ __device__ void orth_item(const Tables& t, int side, const OrthSeg& s, int phase
   }
   __syncthreads();
   const float* G = A;  // rows the Gram is taken of
-  if (phase > 0) {
+  if (RT >= 16 && phase > 0) {
+    // r >= 16: thread per row, the row's r values in registers (one fp32 ->
+    // fp64 conversion each) and W zero-padded to RT x RT in shared memory
+    // (compile-time offsets, broadcast reads), fully unrolled so the r
+    // independent output chains interleave. The element-per-thread loop
+    // below re-reads and re-converts a_k for every output column and runs
+    // each output's dependent chain back to back: r = 32 items of 20-35 us.
+    double* Wp = Gs;  // Gs is free until this item's Gram (last segment)
+    for (int idx = tid; idx < RT * RT; idx += kThreads) {
+      const int k = idx / RT, l = idx - k * RT;
+      Wp[idx] = (k < r && l < r) ? Wm[k * r + l] : 0.0;
+    }
+    __syncthreads();
+    for (int i = tid; i < kSeg; i += kThreads) {
+      double a[RT];
+#pragma unroll
+      for (int k = 0; k < RT; ++k) a[k] = (k < r && i < nr) ? (double)A[k * kLd + i] : 0.0;
+      const int64_t row = s.row0 + i;
+#pragma unroll
+      for (int l0 = 0; l0 < RT; l0 += 4) {
+        float vf[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int l = l0 + u;
+          double v = 0.0;
+#pragma unroll
+          for (int k = 0; k <= l; ++k) v = fma(a[k], Wp[k * RT + l], v);
+          if ((deg >> l) & 1u) v = degenerate_value(seed, s.layer, step, l, row);
+          vf[u] = (i < nr && l < r) ? (float)v : 0.f;
+          B[l * kLd + i] = vf[u];
+          if (i < nr && l < r) F[(int64_t)l * len + row] = vf[u];
+        }
+        if (phase == 2 && t.r8 > 0 && i < nr) {
+          // TC path split copies (Q side k-major [2][R8][m], P side row-major
+          // [2][n][R8]: four consecutive columns -> one 16-byte store each)
+          const int64_t R8 = t.r8;
+          uint32_t hi[4], lo[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) split_tf32(vf[u], hi[u], lo[u]);
+          if (side == 0) {
+            float* d = t.qsplit + L.qs_off;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              if (l0 + u < r) {
+                d[(l0 + u) * len + row] = __uint_as_float(hi[u]);
+                d[(R8 + l0 + u) * len + row] = __uint_as_float(lo[u]);
+              }
+            }
+          } else if (l0 < r) {
+            float* d = t.psplit + L.ps_off;
+            // columns l0 .. l0 + 3 < R8 (R8 is a multiple of 8); beyond r the
+            // split of 0 is 0, as the slot's padding expects
+            *reinterpret_cast<float4*>(d + row * R8 + l0) =
+                make_float4(__uint_as_float(hi[0]), __uint_as_float(hi[1]), __uint_as_float(hi[2]),
+                            __uint_as_float(hi[3]));
+            *reinterpret_cast<float4*>(d + (len + row) * R8 + l0) =
+                make_float4(__uint_as_float(lo[0]), __uint_as_float(lo[1]), __uint_as_float(lo[2]),
+                            __uint_as_float(lo[3]));
+          }
+        }
+      }
+    }
+    if (phase == 2) {
+      __syncthreads();  // smem reuse by the CTA's next item
+      return;
+    }
+    __syncthreads();
+    G = B;
+  } else if (phase > 0) {
     // apply W (upper triangular): out_l = sum_{k<=l} a_k W_kl; a column
     // flagged degenerate becomes the seeded Gaussian column (reading C6)
     for (int idx = tid; idx < r * kSeg; idx += kThreads) {

@@ -5,6 +5,8 @@
 //           E[i,:] = M'[i,:] - P_loc[i,:] Q^T   -- the row stays in registers
 //           between the projection and the residual, so M and E are read once
 //           and E written once (12 B / element); P_loc goes to the P-buffer slot.
+//           ef = 3: projection only (Power-SGD's first projection, Alg. 1
+//           P:180-181, whose residual is formed after the second one): 8 B.
 //   mode 1  K3, P-step decode:  grad[i,:] = scale * P_agg[i,:] Q^T
 //           (write-only stream, 4 B / element).
 //   mode 2  K3, Q-step residual + decode:
@@ -129,7 +131,7 @@ __device__ void k1p_fast(const Tables& t, const LayerDesc& L, const float* __res
       }
     }
     group_sum<R * RT>(acc, G, red, phase);
-    if (ef) {
+    if (ef == 1) {  // ef == 3: Power-SGD projection only (E is updated after Q)
 #pragma unroll
       for (int v = 0; v < V; ++v) {
         const int c = l + v * G;
@@ -343,7 +345,7 @@ __device__ void row_generic(const Tables& t, const LayerDesc& L, float* __restri
       for (int off = 16; off > 0; off >>= 1)
 #pragma unroll
         for (int k = 0; k < RT; ++k) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], off);
-      if (ef) {
+      if (ef == 1) {  // ef == 3: projection only (Power-SGD)
         for (int64_t j = lane; j < m; j += 32) {
           float x = g[j] + e[j];
 #pragma unroll

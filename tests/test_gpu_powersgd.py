@@ -85,24 +85,26 @@ RAGGED = [(1000,), (64, 3, 7, 7), (2, 1024), (1, 8), (3, 9000), (64, 64), (256, 
           (300, 1152), (17,), (130, 20), (512, 4608), (4, 4)]
 
 
-@pytest.mark.parametrize("rank", [1, 2, 4, 8])
+@pytest.mark.parametrize("rank", [1, 2, 4, 8, 16, 32])
 def test_powersgd_split_api_ragged(rank):
+    """r <= 8: the SIMT stream kernels; r = 16 / 32: the register row / column
+    kernels (projection-only row kernel, column kernel, row decode)."""
     inputs = make_inputs(RAGGED, 2, 5, SEED, "lowrank")
     q0 = make_q0(RAGGED, rank, SEED)
     print("worst", _compare(RAGGED, _gpu_split(RAGGED, rank, inputs, q0),
                             _oracle(RAGGED, rank, inputs, q0), inputs))
 
 
-@pytest.mark.parametrize("graphs", [False, True])
-def test_powersgd_step_single_worker(graphs):
+@pytest.mark.parametrize("graphs,rank", [(False, 4), (True, 4), (True, 32)])
+def test_powersgd_step_single_worker(graphs, rank):
     """acp_step at world_size 1 (graph replay and eager) vs the oracle with p = 1;
     the parity argument is ignored."""
     import torch
     from paper_2306_08881_b200 import AcpContext, ACP_POWERSGD
     shapes = [(256, 128), (40,), (64, 147), (1024, 1024)]
     inputs = make_inputs(shapes, 1, 6, SEED, "gaussian")
-    q0 = make_q0(shapes, 4, SEED)
-    ctx = AcpContext(shapes, 4, seed=SEED, q0=q0, flags=ACP_POWERSGD)
+    q0 = make_q0(shapes, rank, SEED)
+    ctx = AcpContext(shapes, rank, seed=SEED, q0=q0, flags=ACP_POWERSGD)
     ctx.set_graphs(graphs)
     gpu = []
     for t, step_in in enumerate(inputs):
@@ -113,12 +115,11 @@ def test_powersgd_step_single_worker(graphs):
                     "E": [{i: ctx.get_state(i)[2].cpu().numpy()
                            for i, s in enumerate(shapes) if len(s) > 1}]})
     ctx.close()
-    _compare(shapes, gpu, _oracle(shapes, 4, inputs, q0), inputs)
+    _compare(shapes, gpu, _oracle(shapes, rank, inputs, q0), inputs)
 
 
 def test_powersgd_rejects_bad_flags():
     from paper_2306_08881_b200 import AcpContext, AcpError, ACP_POWERSGD, ACP_NO_EF
     with pytest.raises(AcpError):
         AcpContext([(64, 64)], 4, flags=ACP_POWERSGD | ACP_NO_EF)
-    with pytest.raises(AcpError):
-        AcpContext([(64, 64)], 16, flags=ACP_POWERSGD)
+
