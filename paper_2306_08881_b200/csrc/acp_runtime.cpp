@@ -116,17 +116,25 @@ struct Plan {
 // the ring's first tile), in byte equivalents, per launch kind: without it
 // CTAs that get many small layers (ResNet) finish last. Measured on 1x B200
 // (profiles/r01_v8_balance.md): 96 KB for the SIMT kernels, 160 KB for the
-// tensor-core K1, 0 for the tensor-core decodes. ACP_SEG_COST_KB overrides.
+// tensor-core K1, 0 for the tensor-core decodes. For the SIMT stream and row
+// kernels the cost grows to 1% of a CTA's share (at most 256 KB) on big
+// models: round 2, two-row K1-P', sweep of the fixed cost -- BERT-L r=4 best
+// at 256 KB (0.947 vs 0.959 ms at 96), ResNet-50 / 152 best at 96 (0.136 /
+// 0.258 vs 0.141 / 0.273 at 256); 1% of the share is ~270 KB for BERT-L and
+// ~20 KB for ResNet-50. ACP_SEG_COST_KB overrides (fixed, every kind).
 enum SegKind { kSegStream = 0, kSegRow = 1, kSegCol = 2, kSegTcK1 = 3, kSegTcDec = 4 };
 double seg_cost_bytes(SegKind k) {
   if (const char* e = std::getenv("ACP_SEG_COST_KB")) return std::atof(e) * 1024.0;
   static const double kb[5] = {96, 96, 96, 160, 0};
   return kb[k] * 1024.0;
 }
+bool seg_cost_adapts(SegKind k) {
+  return !std::getenv("ACP_SEG_COST_KB") && (k == kSegStream || k == kSegRow);
+}
 
 template <class Emit>
 int split_units(const std::vector<Unit>& units, int nsm, double min_share, int max_grid,
-                std::vector<int32_t>& ctab, double seg_cost, Emit emit) {
+                std::vector<int32_t>& ctab, double seg_cost, Emit emit, bool adapt = false) {
   double total = 0;
   for (const Unit& u : units) total += u.cost * (double)u.count + seg_cost;
   if (total <= 0) {
@@ -138,6 +146,13 @@ int split_units(const std::vector<Unit>& units, int nsm, double min_share, int m
   // whole waves: a multiple of the SM count (max_grid is one), so every SM
   // gets the same number of equal shares
   if (grid > nsm && nsm > 0) grid = std::min(max_grid, (grid + nsm - 1) / nsm * nsm);
+  if (adapt) {
+    const double sc = std::min(256.0 * 1024.0, total / grid / 100.0);
+    if (sc > seg_cost) {
+      total += (sc - seg_cost) * (double)units.size();
+      seg_cost = sc;
+    }
+  }
   const double share = (total + seg_cost * grid) / grid;  // + one split segment per CTA
   const size_t cb0 = ctab.size();
   int nseg = 0;
@@ -379,7 +394,7 @@ acp_status build_plan(const acp_config* cfg, Plan& P, bool plan_only = false) {
       s.row0 = a;
       s.row1 = b;
       P.rowsegs.push_back(s);
-    });
+    }, seg_cost_adapts(kSegRow));
     // cta_begin entries are relative to the launch's first segment
     ln.bytes = bytes;
     return ln;
@@ -552,7 +567,7 @@ acp_status build_plan(const acp_config* cfg, Plan& P, bool plan_only = false) {
         part += stride;
       }
       P.streamsegs.push_back(s);
-    });
+    }, seg_cost_adapts(kSegStream));
     if (mode == 3) P.colpart_elems = std::max(P.colpart_elems, part);
     ln.bytes = bytes;
     return ln;
