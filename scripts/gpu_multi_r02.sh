@@ -33,6 +33,7 @@ for W in bert-large-r4 resnet50-r4 bert-large-r32; do
     summ gpurun_out/mg_bench_${N}_${W}_$AR.log
   done
 done
+[ -n "$NO_SWEEP" ] && exit 0
 for BB in 0 1048576 5242880 26214400 104857600 -1; do
   for AR in nccl nvls; do
     P=$((P + 1))
