@@ -128,7 +128,7 @@ __device__ __noinline__ void chol_inv_regs(const Tables& t, const LayerDesc& L, 
 // (non-finite input is an error): it propagates NaN and is
 // reported through `nonfinite`. Out: Rm, Wm (r x r, row-major, W upper
 // triangular with zeros below), dmask (bit k: column k dropped).
-__device__ __forceinline__ void chol_small(const double* Gs, double* Rm, double* Wm, int r,
+__device__ __forceinline__ void chol_small(double* Gs, double* Rm, double* Wm, int r,
                                            uint32_t& dmask, bool& nonfinite) {
   const int lane = threadIdx.x & 31;
   for (int k = 0; k < r; ++k) {
@@ -141,7 +141,11 @@ __device__ __forceinline__ void chol_small(const double* Gs, double* Rm, double*
     const bool fin = isfinite(gkk);
     nonfinite |= !fin;
     const bool dg = fin && (!(gkk > 0.0) || !(d > kDegTol2 * gkk));
-    const double rkk = dg ? 1.0 : sqrt(d);
+    // 1 / R_kk by one reciprocal square root, then products: the column
+    // step's dependent chain no longer holds a sqrt AND a division (the
+    // one-warp Cholesky is most of a small K2 item's latency)
+    const double rinv = dg ? 1.0 : rsqrt(d);
+    const double rkk = dg ? 1.0 : d * rinv;
     if (dg) dmask |= 1u << k;
     if (lane < r) {
       if (dg) {
@@ -150,18 +154,22 @@ __device__ __forceinline__ void chol_small(const double* Gs, double* Rm, double*
       } else if (lane > k) {
         double v = Gs[k * r + lane];
         for (int j = 0; j < k; ++j) v = fma(-Rm[j * r + k], Rm[j * r + lane], v);
-        Rm[k * r + lane] = v / rkk;
+        Rm[k * r + lane] = v * rinv;
       }
       if (lane == k) Rm[k * r + k] = rkk;
     }
     __syncwarp();
+    // G_kk is not read again (later steps read rows k' > k off the
+    // diagonal): keep 1 / R_kk there for the back substitution
+    if (lane == k) Gs[k * r + k] = rinv;
   }
+  __syncwarp();
   if (lane < r) {
     const int l = lane;  // back substitution for column l of W
     for (int i = l; i >= 0; --i) {
       double v = (i == l) ? 1.0 : 0.0;
       for (int j = i + 1; j <= l; ++j) v = fma(-Rm[i * r + j], Wm[j * r + l], v);
-      Wm[i * r + l] = v / Rm[i * r + i];
+      Wm[i * r + l] = v * Gs[i * r + i];
     }
     if ((dmask >> l) & 1u) Wm[l * r + l] = 0.0;
     for (int i = l + 1; i < r; ++i) Wm[i * r + l] = 0.0;
