@@ -49,13 +49,14 @@ __device__ __forceinline__ long long orth_epoch(int64_t step, int phase) { retur
 // not repaired. W = R^-1 column by column in registers (lane l:
 // back substitution, R rows read from shared memory).
 template <int RT>
-__device__ __noinline__ void chol_inv_regs(const Tables& t, const LayerDesc& L, const double* Gs, double* Rm,
+__device__ __noinline__ void chol_inv_regs(const Tables& t, const LayerDesc& L, double* Gs, double* Rm,
                                            double* Wout, int r, int phase, int64_t step) {
   const int l = threadIdx.x & 31;
   double a[RT];  // column l of the (Schur-updated) Gram
 #pragma unroll
   for (int i = 0; i < RT; ++i) a[i] = (i < r && l < r) ? Gs[i * r + l] : 0.0;
   bool mydg = false, nonfinite = false;
+  double myrinv = 1.0;  // 1 / R_ll (lane l)
 #pragma unroll
   for (int k = 0; k < RT; ++k) {
     if (k >= r) break;
@@ -64,13 +65,16 @@ __device__ __noinline__ void chol_inv_regs(const Tables& t, const LayerDesc& L, 
     const bool fin = isfinite(gkk);
     nonfinite |= !fin;
     const bool dg = fin && (!(gkk > 0.0) || !(dkk > kDegTol2 * gkk));
-    const double rkk = dg ? 1.0 : sqrt(dkk);
+    // reciprocal square root + products: no sqrt and division in the chain
+    const double rinv = dg ? 1.0 : rsqrt(dkk);
+    const double rkk = dg ? 1.0 : dkk * rinv;
     double rkl = 0.0;  // R[k][l]
     if (l == k) {
       rkl = rkk;
       mydg = dg;
+      myrinv = rinv;
     } else if (l > k && l < r) {
-      rkl = dg ? 0.0 : a[k] / rkk;
+      rkl = dg ? 0.0 : a[k] * rinv;
     }
     if (l >= k && l < r) Rm[k * r + l] = rkl;
     if (dg && l < k) Rm[l * r + k] = 0.0;  // a dropped column has no entries above R_kk
@@ -80,6 +84,10 @@ __device__ __noinline__ void chol_inv_regs(const Tables& t, const LayerDesc& L, 
       if (l > k) a[i] = fma(-rki, rkl, a[i]);
     }
   }
+  __syncwarp();
+  // the Gram's diagonal is not read again: it holds 1 / R_ii for the
+  // back substitution (independent loads instead of divisions in the chain)
+  if (l < r) Gs[l * r + l] = myrinv;
   __syncwarp();
   // W = R^-1, column l: w[i] = (delta_il - sum_{i<j<=l} R[i][j] w[j]) / R[i][i]
   double w[RT];
@@ -95,10 +103,10 @@ __device__ __noinline__ void chol_inv_regs(const Tables& t, const LayerDesc& L, 
     }
     w[i] = 0.0;
     if (i < r && i <= l && l < r) {
-      const double rii = Rm[i * r + i];
+      const double riinv = Gs[i * r + i];
       // a dropped column l: W_ll = 0 (its output column is replaced by the
       // seeded one); its entries above are 0 either way, since R_il = 0
-      w[i] = (i == l) ? (mydg ? 0.0 : 1.0 / rii) : -(s0 + s1) / rii;
+      w[i] = (i == l) ? (mydg ? 0.0 : riinv) : -(s0 + s1) * riinv;
     }
   }
   if (l < r) {
