@@ -365,37 +365,52 @@ __device__ void orth_item(const Tables& t, int side, const OrthSeg& s, int phase
   const int sp = NP <= kThreads ? tid % S : 0;
   double* part = t.gram + s.gram_off;
   if constexpr (RT >= 16) {
-    // 2 x 2 register blocks over the full RT x RT Gram (RT = 32: one block
-    // per thread; RT = 16: four row splits per block, summed by shuffles):
-    // 4 DFMA per 4 shared loads, four independent accumulation chains
-    constexpr int BPR = RT / 2, NB = BPR * BPR, SB = kThreads / NB;
+    // 4 x 4 register blocks over the full RT x RT Gram (RT = 32: 64 blocks
+    // x 4 row splits; RT = 16: 16 blocks x 16 splits; splits summed by
+    // shuffles): 8 shared loads + 8 fp32 -> fp64 conversions per 16 DFMA.
+    // (2 x 2 blocks took one conversion per DFMA; the F2F rate bound the
+    // r = 32 Gram.) Lanes of a warp read 8 consecutive column blocks at 4
+    // consecutive rows: conflict-free with the padded row stride.
+    constexpr int BS = 4, BPR = RT / BS, NB = BPR * BPR, SB = kThreads / NB;
+    static_assert(NB * SB == kThreads && (SB & (SB - 1)) == 0 && SB <= 32, "Gram block split");
     const int bk = (tid / SB) / BPR, bl = (tid / SB) % BPR, ss = tid % SB;
-    const int k0 = 2 * bk, l0 = 2 * bl;
-    const bool ok0 = k0 < r, ok1 = k0 + 1 < r, ol0 = l0 < r, ol1 = l0 + 1 < r;
-    const float* gk0 = G + (ok0 ? k0 : 0) * kLd;
-    const float* gk1 = G + (ok1 ? k0 + 1 : 0) * kLd;
-    const float* gl0 = G + (ol0 ? l0 : 0) * kLd;
-    const float* gl1 = G + (ol1 ? l0 + 1 : 0) * kLd;
-    double c00 = 0.0, c01 = 0.0, c10 = 0.0, c11 = 0.0;
+    const int k0 = BS * bk, l0 = BS * bl;
+    const float* gk[BS];
+    const float* gl[BS];
+#pragma unroll
+    for (int u = 0; u < BS; ++u) {
+      gk[u] = G + (k0 + u < r ? k0 + u : 0) * kLd;
+      gl[u] = G + (l0 + u < r ? l0 + u : 0) * kLd;
+    }
+    double c[BS][BS];
+#pragma unroll
+    for (int u = 0; u < BS; ++u)
+#pragma unroll
+      for (int v = 0; v < BS; ++v) c[u][v] = 0.0;
     for (int i = ss; i < nr; i += SB) {
-      const double a0 = gk0[i], a1 = gk1[i], b0 = gl0[i], b1 = gl1[i];
-      c00 = fma(a0, b0, c00);
-      c01 = fma(a0, b1, c01);
-      c10 = fma(a1, b0, c10);
-      c11 = fma(a1, b1, c11);
+      double a[BS], b[BS];
+#pragma unroll
+      for (int u = 0; u < BS; ++u) {
+        a[u] = gk[u][i];
+        b[u] = gl[u][i];
+      }
+#pragma unroll
+      for (int u = 0; u < BS; ++u)
+#pragma unroll
+        for (int v = 0; v < BS; ++v) c[u][v] = fma(a[u], b[v], c[u][v]);
     }
 #pragma unroll
-    for (int off = SB / 2; off > 0; off >>= 1) {
-      c00 += __shfl_down_sync(0xffffffffu, c00, off, SB);
-      c01 += __shfl_down_sync(0xffffffffu, c01, off, SB);
-      c10 += __shfl_down_sync(0xffffffffu, c10, off, SB);
-      c11 += __shfl_down_sync(0xffffffffu, c11, off, SB);
-    }
+    for (int off = SB / 2; off > 0; off >>= 1)
+#pragma unroll
+      for (int u = 0; u < BS; ++u)
+#pragma unroll
+        for (int v = 0; v < BS; ++v) c[u][v] += __shfl_down_sync(0xffffffffu, c[u][v], off, SB);
     if (ss == 0) {
-      if (ok0 && ol0) part[k0 * r + l0] = c00;
-      if (ok0 && ol1) part[k0 * r + l0 + 1] = c01;
-      if (ok1 && ol0) part[(k0 + 1) * r + l0] = c10;
-      if (ok1 && ol1) part[(k0 + 1) * r + l0 + 1] = c11;
+#pragma unroll
+      for (int u = 0; u < BS; ++u)
+#pragma unroll
+        for (int v = 0; v < BS; ++v)
+          if (k0 + u < r && l0 + v < r) part[(k0 + u) * r + l0 + v] = c[u][v];
     }
   } else if (NP <= kThreads) {
     const int pi = tid / S;
