@@ -282,8 +282,11 @@ int stream_ctas_per_sm(int mode);
 size_t stream_smem_bytes(int stages, int stage_floats, int factor_floats, int ptile);
 // K2: CholeskyQR2 of the factors named by segs (side 0: Q factors in the
 // Q-buffer, length m; side 1: P factors in the P-buffer, length n).
+// busy_items: items that do work (whole-factor items + 3 per segment);
+// the grid is capped there (the other queue entries are skips).
 cudaError_t launch_orth(int rt, int seg_rows, const Tables& t, int side, const OrthSeg* segs, int nseg,
-                        uint64_t seed, int64_t step, cudaStream_t stream, int* launches);
+                        uint64_t seed, int64_t step, cudaStream_t stream, int* launches,
+                        int busy_items = 0);
 // Fill factor slots with counter-based N(0,1) (tag, step): side as above, or
 // side 2 = Q_0 into the Q-buffer. Layers = all matrices. step < 0: use the
 // device step counter (*t.step). The orthogonaliser reads *t.step and its

@@ -1113,9 +1113,11 @@ acp_status run_orth(acp_ctx* c, int parity, cudaStream_t s) {
   }
   const auto& segs = c->P.orthsegs[side];
   ProfRec* r = prof_begin(c, ACP_K_ORTH, c->P.orth_bytes[side], s);
+  int busy = 0;
+  for (const OrthSeg& sg : segs) busy += sg.local ? 1 : 3;
   cudaError_t e = launch_orth(c->P.RT, c->P.orth_seg[side], c->tab, side,
                               reinterpret_cast<const OrthSeg*>(c->ws + c->P.off_orth[side]),
-                              (int)segs.size(), c->cfg.seed, -1, s, &nl);
+                              (int)segs.size(), c->cfg.seed, -1, s, &nl, busy);
   prof_end(r, s);
   c->launches += nl;
   if (e != cudaSuccess) return cuda_fail(c, e, "orthogonalisation kernel launch");

@@ -724,7 +724,7 @@ __global__ void transpose_kernel(const float* __restrict__ src, float* __restric
 }  // namespace
 
 cudaError_t launch_orth(int rt, int seg_rows, const Tables& t, int side, const OrthSeg* segs, int nseg,
-                        uint64_t seed, int64_t step, cudaStream_t s, int* launches) {
+                        uint64_t seed, int64_t step, cudaStream_t s, int* launches, int busy_items) {
   if (nseg <= 0) return cudaSuccess;
   if (seg_rows != kOrthRowsPerSeg && (seg_rows != kOrthRowsPerSegLarge || rt > 4))
     return cudaErrorInvalidValue;
@@ -737,8 +737,11 @@ cudaError_t launch_orth(int rt, int seg_rows, const Tables& t, int side, const O
     if (e != cudaSuccess) return e;
     int occ = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem);
-    // every CTA must be resident (items wait on each other): at most one wave
-    const int grid = std::max(1, std::min(3 * nseg, nsm * std::max(1, occ)));
+    // every CTA must be resident (items wait on each other): at most one wave;
+    // and no more CTAs than items that do work (whole-factor items leave
+    // two skip entries each in the phase-ordered queue)
+    const int items = busy_items > 0 ? std::min(busy_items, 3 * nseg) : 3 * nseg;
+    const int grid = std::max(1, std::min(items, nsm * std::max(1, occ)));
     kern<<<grid, kThreads, smem, s>>>(t, side, segs, nseg, seed);
     return cudaGetLastError();
   };

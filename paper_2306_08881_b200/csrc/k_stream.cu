@@ -1260,7 +1260,23 @@ __global__ void __launch_bounds__(256) col_reduce_kernel(Tables t, const ColRedu
   const float* base = t.colpart + tk.part_first + (int64_t)k * tk.pc + c;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   const bool vec = ((tk.cols | tk.m | tk.q_dst | tk.ql_dst) & 3) == 0;  // 16-byte aligned rows
-  for (int p = j; p < tk.pcount; p += kSplit) {
+  int p = j;
+  if (vec) {
+    // the slots' loads go out 8 at a time and are summed in slot order (the
+    // same sums as one at a time: bitwise identical), so a unit with many
+    // partial slots costs one L2 round trip per 8 slots, not per slot
+    // (ResNet-50: col_reduce 8 us of a 135 us step)
+    constexpr int kB = 8;
+    for (; p + (kB - 1) * kSplit < tk.pcount; p += kB * kSplit) {
+      float4 v[kB];
+#pragma unroll
+      for (int u = 0; u < kB; ++u)
+        v[u] = __ldcg(reinterpret_cast<const float4*>(base + (int64_t)(p + u * kSplit) * tk.stride));
+#pragma unroll
+      for (int u = 0; u < kB; ++u) acc = f4add(acc, v[u]);
+    }
+  }
+  for (; p < tk.pcount; p += kSplit) {
     const float* src = base + (int64_t)p * tk.stride;
     if (vec) {
       acc = f4add(acc, __ldcg(reinterpret_cast<const float4*>(src)));
