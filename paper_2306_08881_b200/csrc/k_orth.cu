@@ -48,14 +48,15 @@ __device__ __forceinline__ long long orth_epoch(int64_t step, int phase) { retur
 // R_kk = 1, W_kk = 0); a non-finite diagonal raises the sticky flag and is
 // not repaired. W = R^-1 column by column in registers (lane l:
 // back substitution, R rows read from shared memory).
+// The factorisation and inverse (one warp); W goes to Wout (global or shared
+// memory), mydg = column l dropped, nonfinite = a non-finite diagonal seen.
 template <int RT>
-__device__ __noinline__ void chol_inv_regs(const Tables& t, const LayerDesc& L, double* Gs, double* Rm,
-                                           double* Wout, int r, int phase, int64_t step) {
+__device__ __forceinline__ void chol_regs_core(double* Gs, double* Rm, double* Wout, int r, bool& mydg,
+                                               bool& nonfinite) {
   const int l = threadIdx.x & 31;
   double a[RT];  // column l of the (Schur-updated) Gram
 #pragma unroll
   for (int i = 0; i < RT; ++i) a[i] = (i < r && l < r) ? Gs[i * r + l] : 0.0;
-  bool mydg = false, nonfinite = false;
   double myrinv = 1.0;  // 1 / R_ll (lane l)
 #pragma unroll
   for (int k = 0; k < RT; ++k) {
@@ -114,6 +115,14 @@ __device__ __noinline__ void chol_inv_regs(const Tables& t, const LayerDesc& L, 
     for (int i = 0; i < RT; ++i)
       if (i < r) Wout[i * r + l] = (i <= l) ? w[i] : 0.0;
   }
+}
+
+template <int RT>
+__device__ __noinline__ void chol_inv_regs(const Tables& t, const LayerDesc& L, double* Gs, double* Rm,
+                                           double* Wout, int r, int phase, int64_t step) {
+  const int l = threadIdx.x & 31;
+  bool mydg = false, nonfinite = false;
+  chol_regs_core<RT>(Gs, Rm, Wout, r, mydg, nonfinite);
   __threadfence();  // every lane's W columns visible before lane 0 publishes (see orth_item)
   __syncwarp();
   const uint32_t dmask = __ballot_sync(0xffffffffu, mydg && l < r);
@@ -575,7 +584,17 @@ __device__ void orth_local(const Tables& t, int side, const OrthSeg& s, uint64_t
     __syncthreads();
     if (warp == 0) {
       uint32_t dmask = 0;
-      chol_small(Gs, Rm, Wm, r, dmask, nonfinite);
+      if constexpr (RT <= 4) {
+        // register right-looking Cholesky (shuffles, no shared-memory chains):
+        // ResNet-50 K2 26.4 -> 23.9 us, BERT-L r=4 42 -> 39; at RT = 8 its
+        // registers (190) halve the kernel's occupancy and it is slower
+        bool mydg = false;
+        chol_regs_core<RT>(Gs, Rm, Wm, r, mydg, nonfinite);
+        dmask = __ballot_sync(0xffffffffu, mydg && lane < r);
+        __syncwarp();
+      } else {
+        chol_small(Gs, Rm, Wm, r, dmask, nonfinite);
+      }
       if (lane == 0 && pass == 0) *dsh = dmask;
     }
     __syncthreads();
