@@ -338,9 +338,21 @@ def _e2e(res, world, args):
     overlap step t's kernels (PCIe is full duplex), as a training loop would."""
     import torch
     ctx, grads = res["ctx"], res["grads"]
-    sets = [grads, [torch.empty_like(g) for g in grads]]
-    host_in = [g.detach().cpu().pin_memory() for g in grads]
-    host_out = [[torch.empty_like(h).pin_memory() for h in host_in] for _ in range(2)]
+    # the gradients of a step live back to back (16-byte aligned offsets) in
+    # one flat device buffer and one flat pinned host buffer, so each
+    # direction is ONE copy per step (as a DDP-style flat gradient buffer
+    # would be) instead of one small copy per tensor: the per-tensor version
+    # moved BERT-L's ~400 tensors at 34.5 GB/s
+    offs, tot = [], 0
+    for g in grads:
+        offs.append(tot)
+        tot += (g.numel() + 3) // 4 * 4
+    flat_dev = [torch.zeros(tot, device=grads[0].device) for _ in range(2)]
+    sets = [[fd[o:o + g.numel()].view(g.shape) for o, g in zip(offs, grads)] for fd in flat_dev]
+    host_in = torch.zeros(tot).pin_memory()
+    for o, g in zip(offs, grads):
+        host_in[o:o + g.numel()].copy_(g.detach().reshape(-1).cpu())
+    host_out = [torch.empty(tot).pin_memory() for _ in range(2)]
     steps = max(2, min(args.steps, args.e2e_steps))
     comp = torch.cuda.current_stream()
     sh, sd = torch.cuda.Stream(), torch.cuda.Stream()
@@ -352,8 +364,7 @@ def _e2e(res, world, args):
         with torch.cuda.stream(sh):
             if d_done[b] is not None:
                 sh.wait_event(d_done[b])  # step t-2's download has read this set
-            for h, g in zip(host_in, sets[b]):
-                g.copy_(h, non_blocking=True)
+            flat_dev[b].copy_(host_in, non_blocking=True)
             e = ev()
             e.record(sh)
         return e
@@ -366,8 +377,7 @@ def _e2e(res, world, args):
         c.record(comp)
         with torch.cuda.stream(sd):
             sd.wait_event(c)
-            for g, h in zip(sets[b], host_out[b]):
-                h.copy_(g, non_blocking=True)
+            host_out[b].copy_(flat_dev[b], non_blocking=True)
             d = ev()
             d.record(sd)
         d_done[b] = d
@@ -390,8 +400,9 @@ def _e2e(res, world, args):
     ms = max_over_ranks(e0.elapsed_time(e1) / steps)
     nbytes = 4 * res["nel"]
     return {"value": world * nbytes / (ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": ms,
-            "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "steps": steps,
-            "pipelined": "H2D(t+1) and D2H(t) overlap step t (two gradient sets, copy streams)"}
+            "h2d_bytes_per_step": 4 * tot, "d2h_bytes_per_step": 4 * tot, "steps": steps,
+            "pipelined": "H2D(t+1) and D2H(t) overlap step t (two flat gradient buffers, one copy per "
+                         "direction per step, copy streams)"}
 
 
 def _nvlink(prof, world):
